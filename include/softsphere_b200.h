@@ -1,0 +1,210 @@
+/*
+ * softsphere_b200.h -- C ABI of the B200-native sphere-render hot path.
+ *
+ * The reference (`softsphere`, pure NumPy) has no FFI; this header declares the entry
+ * points a reference-side binding for the render path would bind.  Each one names the
+ * reference interface it replaces (paths relative to pkg/src/softsphere/):
+ *
+ *   ss_forward   <- render_forward     raster.py:437-512  (compute_bounds :181-236,
+ *                                      sort_draw_records :239-244, _bin_tiles :267-293,
+ *                                      _draw_tile :328-417)
+ *   ss_backward  <- render_backward    grad.py:323-357    (_hit_gradients :89-179,
+ *                                      _accumulate_tiles :210-259,
+ *                                      accumulate_and_normalize :262-302,
+ *                                      gate_small_spheres :305-320)
+ *   ss_workspace_bytes / SsDims        the arrays render_forward allocates per call
+ *                                      (raster.py:462-474) become one caller-owned buffer
+ *   ss_read_status                     RenderStats raster.py:113-123 + the ValidationError
+ *                                      conditions of SphereScene.validate scene.py:91-114
+ *   ss_debug_tile_lists                (record_seq, tile_starts) of _bin_tiles, parity only
+ *
+ * Conventions (camera.py:3-13): p_cam = R (p_world - t), camera looks down +z, pixel
+ * (i, j) centre ray through u = i + 0.5, v = j + 0.5, NDC z = (far - depth)/(far - near).
+ *
+ * Everything is plain pointers and sizes; no torch types.  All data pointers are DEVICE
+ * pointers unless marked host.  The library never allocates, frees or synchronises
+ * (except ss_read_status); all work is enqueued on the caller's stream.
+ */
+#ifndef SOFTSPHERE_B200_H
+#define SOFTSPHERE_B200_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define SS_ABI_VERSION 1
+
+/* ---- return codes (host-side argument checking; errors.py classes in parentheses) ---- */
+#define SS_OK 0
+#define SS_ERR_NULL 1         /* a required pointer is NULL */
+#define SS_ERR_DIMS 2         /* bad dims: M < 0, d outside 1..32, W/H outside 1..16384 (ConfigurationError) */
+#define SS_ERR_PARAMS 3       /* eps <= 0, tau outside [0,1), top_k outside 1..64 (ValidationError, blend.py:40-45) */
+#define SS_ERR_CAMERA 4       /* focal/sensor <= 0, near >= far, bad mode (ConfigurationError, camera.py:153-177) */
+#define SS_ERR_WORKSPACE 5    /* workspace_bytes < ss_workspace_bytes(dims) */
+#define SS_ERR_UNSUPPORTED 6  /* tile != 16 or chunk outside 1..256 */
+#define SS_ERR_CUDA 7         /* a CUDA runtime call failed (see ss_last_cuda_error) */
+
+/* ---- device-side status flags (status[0], read with ss_read_status) ---- */
+#define SS_FLAG_INVALID_INPUT 1u  /* NaN/Inf field or radius <= 0 (ValidationError, scene.py:91-114) */
+#define SS_FLAG_PAIR_OVERFLOW 2u  /* tile-sphere pairs > dims.max_pairs; nothing was drawn */
+
+/* ---- option flags ---- */
+#define SS_OPT_STORE_BUFFER 1u   /* forward: write ids/z/closeness/log_denom (store_buffer, raster.py:445) */
+#define SS_OPT_COLLECT_STATS 2u  /* forward: fill candidates_tested/hits_blended/pixels_early_stopped */
+#define SS_OPT_NORMALIZE 4u      /* backward: normalize=True (grad.py:331) */
+#define SS_OPT_GATE 8u           /* backward: gate=True (grad.py:332) */
+#define SS_OPT_CAMERA_GRADS 16u  /* backward: also reduce camera gradients */
+#define SS_OPT_ACCUMULATE 32u    /* backward: add into d_* / pixel_count instead of overwriting (multi-view) */
+#define SS_OPT_REUSE_RECORDS 64u /* backward: camera-frame records in the workspace are still those of the
+                                    matching forward call; skip recomputing them (grad.py:213, :351) */
+#define SS_OPT_SKIP_VALIDATE 128u /* forward: do not scan inputs for NaN/Inf/radius <= 0 */
+
+#define SS_MODE_PINHOLE 0
+#define SS_MODE_ORTHOGRAPHIC 1
+
+#define SS_MAX_FEATURE_DIM 32
+#define SS_MAX_TOP_K 64
+#define SS_TILE 16
+#define SS_MAX_CHUNK 256
+
+/* Camera (camera.py:130-177), passed by value from the host. */
+typedef struct SsCamera {
+    double t[3];      /* camera position in world units */
+    double R[9];      /* row-major rotation, p_cam = R (p - t) */
+    double focal;     /* focal_length */
+    double sensor_w;  /* sensor_width; pixel size = sensor_w / width */
+    double near_;     /* min depth */
+    double far_;      /* max depth */
+    int32_t width;
+    int32_t height;
+    int32_t mode;     /* SS_MODE_* */
+    int32_t pad_;
+} SsCamera;
+
+/* Problem size; fixes the workspace layout. */
+typedef struct SsDims {
+    int64_t num_spheres;  /* M */
+    int64_t max_pairs;    /* capacity for (tile, sphere) pairs, < 2^31 */
+    int32_t feature_dim;  /* d, 1..32 */
+    int32_t width;        /* W */
+    int32_t height;       /* H */
+    int32_t top_k;        /* K = n_track, 1..64 */
+} SsDims;
+
+/* BlendParams (blend.py:25-45) + pipeline knobs of render_forward (raster.py:437-447). */
+typedef struct SsBlend {
+    double gamma;   /* clamped to [1e-5, 1] by the library, like BlendParams.__post_init__ */
+    double eps;     /* epsilon > 0 */
+    double tau;     /* in [0, 1); 0 disables early stopping */
+    int32_t tile;   /* must be 16 */
+    int32_t chunk;  /* candidates per vote/batch, 1..256 (reference default 256) */
+    uint32_t flags; /* SS_OPT_* */
+    uint32_t pad_;
+} SsBlend;
+
+/*
+ * Forward.  Inputs are float32 SoA tensors (the reference holds float64 columns of the
+ * same values): pos (M,3), rad (M), opa (M, raw/unclamped), feat (M,d), bg (d).
+ * Outputs: image (H,W,d), bg_weight (H,W) and -- with SS_OPT_STORE_BUFFER -- the backward
+ * buffer in SLOT-MAJOR layout: ids/z/closeness are (K,H,W) (the reference's (H,W,K)
+ * transposed so that pixel-parallel access is coalesced), log_denom (H,W).
+ * Empty slots: id -1, z 0, closeness 0 (raster.py:410-413).
+ * Optional parity outputs (NULL to skip): rect (M,4) int32 = x_min,x_max,y_min,y_max;
+ * on_sensor (M) uint8; earliest (M) float64; proj_radius_px (M) float64.
+ */
+typedef struct SsForwardArgs {
+    SsDims dims;
+    SsCamera cam;
+    SsBlend blend;
+    const float *pos, *rad, *opa, *feat, *bg;
+    void *workspace;
+    size_t workspace_bytes;
+    float *image;
+    float *bg_weight;
+    int32_t *ids;
+    float *z;
+    float *closeness;
+    float *log_denom;
+    int32_t *rect;
+    uint8_t *on_sensor;
+    double *earliest;
+    double *proj_radius_px;
+} SsForwardArgs;
+
+/*
+ * Backward.  Consumes the buffer written by ss_forward and upstream (H,W,d).
+ * Outputs: d_pos (M,3), d_rad (M), d_opa (M), d_feat (M,d) float32; pixel_count (M) int32;
+ * cam_grad: 16 float64 on the device = d_translation[3], G[9] (= d loss / d R, row-major,
+ * to be pulled back through the rotation parameterisation by the host, camera.py:57-117),
+ * d_focal, d_sensor_width, 2 reserved.  cam_grad may be NULL without SS_OPT_CAMERA_GRADS.
+ */
+typedef struct SsBackwardArgs {
+    SsDims dims;
+    SsCamera cam;
+    SsBlend blend;
+    const float *pos, *rad, *opa, *feat, *bg;
+    void *workspace;
+    size_t workspace_bytes;
+    const int32_t *ids;
+    const float *z;
+    const float *closeness;
+    const float *log_denom;
+    const float *upstream;
+    float *d_pos;
+    float *d_rad;
+    float *d_opa;
+    float *d_feat;
+    int32_t *pixel_count;
+    double *cam_grad;
+} SsBackwardArgs;
+
+/* status block, host copy (ss_read_status) */
+typedef struct SsStatus {
+    int64_t flags;                 /* SS_FLAG_* */
+    int64_t spheres_on_sensor;     /* RenderStats.spheres_on_sensor */
+    int64_t num_pairs;             /* tile-sphere pairs the scene needs (T) */
+    int64_t candidates_tested;     /* RenderStats.candidates_tested (SS_OPT_COLLECT_STATS) */
+    int64_t hits_blended;          /* RenderStats.hits_blended */
+    int64_t pixels_early_stopped;  /* RenderStats.pixels_early_stopped */
+    int64_t first_invalid;         /* lowest sphere index that failed validation, or -1 */
+    int64_t reserved[9];
+} SsStatus;
+
+int ss_abi_version(void);
+const char *ss_status_string(int code);
+const char *ss_last_cuda_error(void);
+
+/* Bytes of caller-owned device workspace for `dims` (256-byte aligned base required). */
+int ss_workspace_bytes(const SsDims *dims, size_t *out_bytes);
+
+/* `stream` is a cudaStream_t passed as void* (NULL = default stream). */
+int ss_forward(const SsForwardArgs *args, void *stream);
+int ss_backward(const SsBackwardArgs *args, void *stream);
+
+/* Copies the status block of the last forward on `workspace` to the host; synchronises `stream`. */
+int ss_read_status(const void *workspace, SsStatus *out_host, void *stream);
+
+/* Parity/debug: copy the per-tile candidate lists of the last forward (sphere ids grouped by
+ * tile in scan order) into tile_starts_out (n_tiles + 1, int32) and ids_out (max_pairs, int32). */
+int ss_debug_tile_lists(const SsDims *dims, const void *workspace, int32_t *tile_starts_out,
+                        int32_t *ids_out, void *stream);
+
+/* Number of kernels this library has launched in this process (bench.py's gpu_launches). */
+int64_t ss_launch_count(void);
+
+/* Measurement only (no reference counterpart): when enabled, every kernel the library launches
+ * is bracketed by a CUDA event pair on the launching stream.  ss_profile_collect synchronises
+ * the device and returns, per kernel id, the summed duration in ms and the launch count since
+ * the last enable/collect. */
+void ss_profile_enable(int on);
+int ss_profile_collect(double *ms_sum, int64_t *launches, int n);
+int ss_profile_kernel_count(void);
+const char *ss_profile_kernel_name(int kid);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* SOFTSPHERE_B200_H */

@@ -1,0 +1,15 @@
+"""B200-native differentiable sphere renderer (Pulsar hot path: forward + backward).
+
+The host types and the reference-facing functions import without a GPU; anything that renders
+needs the sm_100a library (csrc/libss_b200.so) and a CUDA device -- there is no fallback.
+"""
+from .types import (AXIS_ANGLE, ORTHOGRAPHIC, PINHOLE, SIX_D, BackwardBuffer, BlendParams, Camera,
+                    CameraGradients, ConfigurationError, ContractViolation, DivergenceError, FeatureImage,
+                    FormatError, RenderStats, SceneGradients, SoftSphereError, SphereScene, ValidationError,
+                    add_sphere_arrays, axis_angle_to_matrix, axis_angle_vjp, camera_from_vector,
+                    camera_to_vector, new_scene, rotation_6d_vjp, rotation_from_6d)
+from .api import SoftsphereAdapter, render_backward, render_forward
+from .engine import CameraSpec, RenderEngine, default_engine
+from .function import Renderer, SphereRender
+
+__version__ = "0.1.0"

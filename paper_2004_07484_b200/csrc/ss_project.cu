@@ -1,0 +1,396 @@
+// Step 0 + tile binning for sm_100a.
+//
+//   k_project   reference compute_bounds (raster.py:181-236): world->camera, tangent-wedge
+//               extents, pixel rectangles, culling, earliest depth, projected radius, input
+//               validation (scene.py:91-114) -- float64 per sphere, M-parallel, plus the
+//               per-tile candidate COUNT (one atomic per touched tile).
+//   k_scan      exclusive prefix sum of the tile counts -> tile_start (raster.py:290-292).
+//   k_emit      writes each (tile, sphere) pair into its tile's segment.
+//   k_tile_sort per-tile sort of the segment by (earliest float64, sphere index): exactly the
+//               order the reference gets from "stable argsort by earliest" (raster.py:243)
+//               followed by "stable argsort by tile id" (raster.py:289).  One CTA per tile,
+//               bitonic network in shared memory; the global M-wide sort and the T-wide
+//               (tile, depth) radix sort of the classic design are not needed.
+#include <math.h>
+
+#include "ss_common.cuh"
+
+namespace ss {
+
+namespace {
+
+constexpr double kHalfPi = 1.57079632679489661923;
+constexpr double kIntHuge = 1073741824.0;  // 1 << 30 (raster.py:34)
+
+__device__ __forceinline__ double clampd(double x, double lo, double hi) {
+    return fmin(fmax(x, lo), hi);
+}
+
+// raster.py:130-154
+__device__ void axis_extent_pinhole(double ca, double cz, double r, double focal, double &lo,
+                                    double &hi, bool &empty) {
+    double n2 = ca * ca + cz * cz;
+    double n = sqrt(n2);
+    bool full = n2 <= r * r;
+    double beta = asin(clampd(r / fmax(n, 1e-300), 0.0, 1.0));
+    double phi = atan2(ca, cz);
+    double lo_a = phi - beta, hi_a = phi + beta;
+    empty = ((lo_a >= kHalfPi) || (hi_a <= -kHalfPi)) && !full;
+    const double cap = kHalfPi - 1e-9;
+    lo = (lo_a <= -kHalfPi) ? -INFINITY : focal * tan(clampd(lo_a, -cap, cap));
+    hi = (hi_a >= kHalfPi) ? INFINITY : focal * tan(clampd(hi_a, -cap, cap));
+    if (full) { lo = -INFINITY; hi = INFINITY; }
+}
+
+// raster.py:157-178
+__device__ void discretize_extent(double lo_px, double hi_px, double center_px, int limit, int &i_lo,
+                                  int &i_hi, bool &outside) {
+    double pad = 1e-9 * (1.0 + fabs(lo_px));
+    double lo_f = clampd(ceil(lo_px - 0.5 - pad), -kIntHuge, kIntHuge);
+    pad = 1e-9 * (1.0 + fabs(hi_px));
+    double hi_f = clampd(floor(hi_px - 0.5 + pad), -kIntHuge, kIntHuge);
+    long long a = (long long)lo_f, b = (long long)hi_f;
+    if (a > b) {
+        double c = isfinite(center_px) ? center_px : 0.0;
+        long long nearest = (long long)clampd(floor(c), -kIntHuge, kIntHuge);
+        a = nearest; b = nearest;
+    }
+    outside = (b < 0) || (a > limit - 1);
+    a = a < 0 ? 0 : (a > limit - 1 ? limit - 1 : a);
+    b = b < 0 ? 0 : (b > limit - 1 ? limit - 1 : b);
+    i_lo = (int)a; i_hi = (int)b;
+}
+
+__device__ __forceinline__ unsigned long long order_key(double e) {
+    e += 0.0;  // -0.0 -> +0.0 so that equal values have equal keys
+    unsigned long long b = (unsigned long long)__double_as_longlong(e);
+    return (b >> 63) ? ~b : (b | 0x8000000000000000ull);
+}
+
+struct ProjectArgs {
+    long long M; int d;
+    const float *pos, *rad, *opa, *feat, *bg;
+    Cam cam;
+    Rec *rec; unsigned long long *key; ushort4 *trect; double *proj_r;
+    int *tile_count; long long *status;
+    int32_t *rect; uint8_t *on_sensor; double *earliest; double *proj_r_out;
+    int records_only; int validate;
+};
+
+__global__ void __launch_bounds__(256) k_project(ProjectArgs a) {
+    long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+    bool in = i < a.M;
+    bool on = false;
+    if (in) {
+        const Cam &cam = a.cam;
+        float pxf = a.pos[3 * i], pyf = a.pos[3 * i + 1], pzf = a.pos[3 * i + 2];
+        float rf = a.rad[i], of = a.opa[i];
+        bool bad = false;
+        if (a.validate) {
+            bad = !(isfinite(pxf) && isfinite(pyf) && isfinite(pzf) && isfinite(rf) && isfinite(of)) ||
+                  !(rf > 0.0f);
+            const float *f = a.feat + (size_t)i * a.d;
+            for (int k = 0; k < a.d; ++k) bad |= !isfinite(f[k]);
+            if (i == 0)
+                for (int k = 0; k < a.d; ++k) bad |= !isfinite(a.bg[k]);
+            if (bad) {
+                atomicOr((unsigned long long *)&a.status[ST_FLAGS], (unsigned long long)SS_FLAG_INVALID_INPUT);
+                atomicMax(&a.status[ST_FIRST_INVALID], a.M - i);  // decoded by k_scan
+            }
+        }
+        double dx = (double)pxf - cam.t[0], dy = (double)pyf - cam.t[1], dz = (double)pzf - cam.t[2];
+        const double *R = cam.R;
+        double cx = dx * R[0] + dy * R[1] + dz * R[2];
+        double cy = dx * R[3] + dy * R[4] + dz * R[5];
+        double cz = dx * R[6] + dy * R[7] + dz * R[8];
+        double r = (double)rf;
+        Rec rc; rc.cx = cx; rc.cy = cy; rc.cz = cz; rc.r = rf; rc.o = fminf(fmaxf(of, 0.0f), 1.0f);
+        a.rec[i] = rc;
+
+        double lo_x, hi_x, lo_y, hi_y, u_c, v_c, e, pr;
+        bool empty_x = false, empty_y = false;
+        bool behind = (cz + r) <= 0.0;
+        int w = cam.W, h = cam.H;
+        if (cam.mode == SS_MODE_PINHOLE) {
+            axis_extent_pinhole(cx, cz, r, cam.focal, lo_x, hi_x, empty_x);
+            axis_extent_pinhole(cy, cz, r, cam.focal, lo_y, hi_y, empty_y);
+            double safe_z = cz > 0.0 ? cz : INFINITY;
+            u_c = w / 2.0 + cam.focal * cx / safe_z * cam.ppu;
+            v_c = h / 2.0 + cam.focal * cy / safe_z * cam.ppu;
+            double d2 = cx * cx + cy * cy + cz * cz;
+            e = sqrt(d2) - r;
+            pr = (cam.focal * r / sqrt(fmax(d2 - r * r, 1e-300))) * cam.ppu;
+            if (d2 <= r * r) pr = (double)(w > h ? w : h);
+        } else {
+            lo_x = cx - r; hi_x = cx + r; lo_y = cy - r; hi_y = cy + r;
+            u_c = w / 2.0 + cx * cam.ppu;
+            v_c = h / 2.0 + cy * cam.ppu;
+            e = cz - r;
+            pr = r * cam.ppu;
+        }
+        a.proj_r[i] = pr;
+        if (a.proj_r_out) a.proj_r_out[i] = pr;
+        if (!a.records_only) {
+            int x0, x1, y0, y1; bool out_x, out_y;
+            discretize_extent(w / 2.0 + lo_x * cam.ppu, w / 2.0 + hi_x * cam.ppu, u_c, w, x0, x1, out_x);
+            discretize_extent(h / 2.0 + lo_y * cam.ppu, h / 2.0 + hi_y * cam.ppu, v_c, h, y0, y1, out_y);
+            on = !(behind || empty_x || empty_y || out_x || out_y) && !bad;
+            if (!on) e = INFINITY;
+            if (a.rect) {
+                a.rect[4 * i] = x0; a.rect[4 * i + 1] = x1; a.rect[4 * i + 2] = y0; a.rect[4 * i + 3] = y1;
+            }
+            if (a.on_sensor) a.on_sensor[i] = on ? 1 : 0;
+            if (a.earliest) a.earliest[i] = e;
+            a.key[i] = order_key(e);
+            ushort4 tr;
+            if (on) {
+                tr.x = (unsigned short)(x0 / TILE); tr.y = (unsigned short)(x1 / TILE);
+                tr.z = (unsigned short)(y0 / TILE); tr.w = (unsigned short)(y1 / TILE);
+                for (int ty = tr.z; ty <= tr.w; ++ty)
+                    for (int tx = tr.x; tx <= tr.y; ++tx) atomicAdd(&a.tile_count[ty * cam.ntx + tx], 1);
+            } else {
+                tr.x = 1; tr.y = 0; tr.z = 1; tr.w = 0;
+            }
+            a.trect[i] = tr;
+        }
+    }
+    if (!a.records_only) {
+        unsigned m = __ballot_sync(0xffffffffu, on);
+        if ((threadIdx.x & 31) == 0 && m)
+            atomicAdd((unsigned long long *)&a.status[ST_ON_SENSOR], (unsigned long long)__popc(m));
+    }
+}
+
+// Single-CTA exclusive scan over the tile counts; also resets the emit cursors, lists the
+// tiles whose segment is too long for the small sort kernel, and publishes T / overflow.
+__global__ void __launch_bounds__(1024) k_scan(const int *__restrict__ tile_count, int *tile_start,
+                                               int *tile_cursor, int *big_tiles, int n_tiles,
+                                               long long max_pairs, long long M, long long *status) {
+    __shared__ long long warp_sums[32];
+    __shared__ long long carry_s;
+    __shared__ int n_big;
+    int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
+    if (tid == 0) { carry_s = 0; n_big = 0; }
+    __syncthreads();
+    for (int base = 0; base < n_tiles; base += 1024) {
+        int i = base + tid;
+        int c = i < n_tiles ? tile_count[i] : 0;
+        long long v = c;
+        for (int o = 1; o < 32; o <<= 1) {
+            long long n = __shfl_up_sync(0xffffffffu, v, o);
+            if (lane >= o) v += n;
+        }
+        if (lane == 31) warp_sums[wid] = v;
+        __syncthreads();
+        if (wid == 0) {
+            long long s = warp_sums[lane];
+            for (int o = 1; o < 32; o <<= 1) {
+                long long n = __shfl_up_sync(0xffffffffu, s, o);
+                if (lane >= o) s += n;
+            }
+            warp_sums[lane] = s;
+        }
+        __syncthreads();
+        long long carry = carry_s;
+        long long excl = carry + (wid ? warp_sums[wid - 1] : 0) + v - c;
+        if (i < n_tiles) {
+            tile_start[i] = (int)(excl > 0x7fffffffLL ? 0x7fffffffLL : excl);
+            tile_cursor[i] = 0;
+            if (c > SORT_SMALL) big_tiles[1 + atomicAdd(&n_big, 1)] = i;
+        }
+        __syncthreads();
+        if (tid == 0) carry_s = carry + warp_sums[31];
+        __syncthreads();
+    }
+    if (tid == 0) {
+        long long total = carry_s;
+        tile_start[n_tiles] = (int)(total > 0x7fffffffLL ? 0x7fffffffLL : total);
+        big_tiles[0] = n_big;
+        status[ST_PAIRS] = total;
+        if (total > max_pairs) status[ST_FLAGS] |= SS_FLAG_PAIR_OVERFLOW;
+        long long enc = status[ST_FIRST_INVALID];
+        status[ST_FIRST_INVALID] = enc ? M - enc : -1;
+    }
+}
+
+__global__ void __launch_bounds__(256) k_emit(long long M, const ushort4 *__restrict__ trect,
+                                              const unsigned long long *__restrict__ key,
+                                              const int *__restrict__ tile_start, int *tile_cursor,
+                                              unsigned long long *pair_key, int *pair_id, int ntx,
+                                              const long long *__restrict__ status) {
+    if (status[ST_FLAGS] & SS_FLAG_PAIR_OVERFLOW) return;
+    long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= M) return;
+    ushort4 tr = trect[i];
+    if (tr.x > tr.y) return;
+    unsigned long long k = key[i];
+    for (int ty = tr.z; ty <= tr.w; ++ty)
+        for (int tx = tr.x; tx <= tr.y; ++tx) {
+            int t = ty * ntx + tx;
+            int slot = tile_start[t] + atomicAdd(&tile_cursor[t], 1);
+            pair_key[slot] = k;
+            pair_id[slot] = (int)i;
+        }
+}
+
+// ---- per-tile sort -------------------------------------------------------------------
+// Bitonic network in the "all comparators ascending" form: merge step k first compares
+// i with i ^ (k-1) (flip), then i with i ^ j for j = k/4 ... 1 (disperse).  Because every
+// comparator moves the minimum to the lower index, elements beyond n behave like +inf
+// without being stored: comparators whose upper index is >= n are skipped.
+
+__device__ __forceinline__ bool pair_less(unsigned long long ka, int ia, unsigned long long kb, int ib) {
+    return ka < kb || (ka == kb && ia < ib);
+}
+
+template <typename KeyPtr, typename IdPtr>
+__device__ __forceinline__ void cas(KeyPtr keys, IdPtr ids, int l, int r) {
+    unsigned long long kl = keys[l], kr = keys[r];
+    int il = ids[l], ir = ids[r];
+    if (pair_less(kr, ir, kl, il)) { keys[l] = kr; keys[r] = kl; ids[l] = ir; ids[r] = il; }
+}
+
+template <typename KeyPtr, typename IdPtr>
+__device__ void bitonic_sort_cta(KeyPtr keys, IdPtr ids, int n) {
+    int np2 = 1;
+    while (np2 < n) np2 <<= 1;
+    int half = np2 >> 1;
+    for (int k = 2; k <= np2; k <<= 1) {
+        int hk = k >> 1;
+        for (int c = threadIdx.x; c < half; c += blockDim.x) {  // flip
+            int p = c & (hk - 1);
+            int base = (c - p) << 1;
+            int l = base + p, r = base + k - 1 - p;
+            if (r < n) cas(keys, ids, l, r);
+        }
+        __syncthreads();
+        for (int j = hk >> 1; j >= 1; j >>= 1) {  // disperse
+            for (int c = threadIdx.x; c < half; c += blockDim.x) {
+                int p = c & (j - 1);
+                int l = ((c - p) << 1) + p, r = l + j;
+                if (r < n) cas(keys, ids, l, r);
+            }
+            __syncthreads();
+        }
+    }
+}
+
+__global__ void __launch_bounds__(256) k_tile_sort_small(const int *__restrict__ tile_start,
+                                                         const unsigned long long *__restrict__ pair_key,
+                                                         int *pair_id, const long long *__restrict__ status) {
+    __shared__ unsigned long long keys[SORT_SMALL];
+    __shared__ int ids[SORT_SMALL];
+    if (status[ST_FLAGS] & SS_FLAG_PAIR_OVERFLOW) return;
+    int t = blockIdx.x;
+    int s0 = tile_start[t], n = tile_start[t + 1] - s0;
+    if (n < 2 || n > SORT_SMALL) return;
+    for (int i = threadIdx.x; i < n; i += blockDim.x) { keys[i] = pair_key[s0 + i]; ids[i] = pair_id[s0 + i]; }
+    __syncthreads();
+    bitonic_sort_cta(keys, ids, n);
+    for (int i = threadIdx.x; i < n; i += blockDim.x) pair_id[s0 + i] = ids[i];
+}
+
+// Persistent over the list of long segments: <= SORT_BIG in dynamic smem, longer in place.
+__global__ void __launch_bounds__(256) k_tile_sort_big(const int *__restrict__ tile_start,
+                                                       unsigned long long *pair_key, int *pair_id,
+                                                       const int *__restrict__ big_tiles,
+                                                       const long long *__restrict__ status) {
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    unsigned long long *keys = (unsigned long long *)smem_raw;
+    int *ids = (int *)(smem_raw + (size_t)SORT_BIG * 8);
+    if (status[ST_FLAGS] & SS_FLAG_PAIR_OVERFLOW) return;
+    int n_big = big_tiles[0];
+    for (int b = blockIdx.x; b < n_big; b += gridDim.x) {
+        int t = big_tiles[1 + b];
+        int s0 = tile_start[t], n = tile_start[t + 1] - s0;
+        if (n <= SORT_BIG) {
+            for (int i = threadIdx.x; i < n; i += blockDim.x) { keys[i] = pair_key[s0 + i]; ids[i] = pair_id[s0 + i]; }
+            __syncthreads();
+            bitonic_sort_cta(keys, ids, n);
+            for (int i = threadIdx.x; i < n; i += blockDim.x) pair_id[s0 + i] = ids[i];
+            __syncthreads();
+        } else {
+            __syncthreads();
+            bitonic_sort_cta(pair_key + s0, pair_id + s0, n);  // global memory, one CTA: slow but exact
+        }
+    }
+}
+
+}  // namespace
+
+cudaError_t launch_project(const FwdLaunch &a, bool records_only, cudaStream_t s) {
+    long long M = a.dims.num_spheres;
+    char *ws = a.ws;
+    const Layout &L = a.L;
+    if (!records_only) {
+        // status + tile_count are contiguous: one memset
+        ProfScope ps(KID_MEMSET_FWD, s);
+        cudaError_t e = cudaMemsetAsync(ws + L.status, 0, L.tile_start - L.status, s);
+        if (e != cudaSuccess) return e;
+    }
+    if (M > 0) {
+        ProjectArgs p;
+        p.M = M; p.d = a.dims.feature_dim;
+        p.pos = a.pos; p.rad = a.rad; p.opa = a.opa; p.feat = a.feat; p.bg = a.bg;
+        p.cam = a.cam;
+        p.rec = (Rec *)(ws + L.rec); p.key = (unsigned long long *)(ws + L.key);
+        p.trect = (ushort4 *)(ws + L.trect); p.proj_r = (double *)(ws + L.proj_r);
+        p.tile_count = (int *)(ws + L.tile_count); p.status = (long long *)(ws + L.status);
+        p.rect = a.rect; p.on_sensor = a.on_sensor; p.earliest = a.earliest; p.proj_r_out = a.proj_r_out;
+        p.records_only = records_only ? 1 : 0;
+        p.validate = (!records_only && !(a.blend.flags & SS_OPT_SKIP_VALIDATE)) ? 1 : 0;
+        unsigned grid = (unsigned)((M + 255) / 256);
+        ProfScope ps(KID_PROJECT, s);
+        k_project<<<grid, 256, 0, s>>>(p);
+        count_launch();
+    }
+    return cudaGetLastError();
+}
+
+cudaError_t launch_binning(const FwdLaunch &a, cudaStream_t s) {
+    long long M = a.dims.num_spheres;
+    char *ws = a.ws;
+    const Layout &L = a.L;
+    int *tile_start = (int *)(ws + L.tile_start);
+    int *tile_cursor = (int *)(ws + L.tile_cursor);
+    int *big_tiles = (int *)(ws + L.big_tiles);
+    long long *status = (long long *)(ws + L.status);
+    unsigned long long *pair_key = (unsigned long long *)(ws + L.pair_key);
+    int *pair_id = (int *)(ws + L.pair_id);
+    {
+        ProfScope ps(KID_SCAN, s);
+        k_scan<<<1, 1024, 0, s>>>((const int *)(ws + L.tile_count), tile_start, tile_cursor, big_tiles,
+                                  L.n_tiles, a.dims.max_pairs, M, status);
+    }
+    count_launch();
+    if (M > 0) {
+        unsigned grid = (unsigned)((M + 255) / 256);
+        {
+            ProfScope ps(KID_EMIT, s);
+            k_emit<<<grid, 256, 0, s>>>(M, (const ushort4 *)(ws + L.trect),
+                                        (const unsigned long long *)(ws + L.key), tile_start, tile_cursor,
+                                        pair_key, pair_id, L.ntx, status);
+        }
+        {
+            ProfScope ps(KID_SORT_SMALL, s);
+            k_tile_sort_small<<<L.n_tiles, 256, 0, s>>>(tile_start, pair_key, pair_id, status);
+        }
+        static bool attr_set = false;
+        size_t big_smem = (size_t)SORT_BIG * 12;
+        if (!attr_set) {
+            cudaError_t e = cudaFuncSetAttribute(k_tile_sort_big, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                                 (int)big_smem);
+            if (e != cudaSuccess) return e;
+            attr_set = true;
+        }
+        int grid_big = L.n_tiles < 296 ? L.n_tiles : 296;
+        {
+            ProfScope ps(KID_SORT_BIG, s);
+            k_tile_sort_big<<<grid_big, 256, big_smem, s>>>(tile_start, pair_key, pair_id, big_tiles, status);
+        }
+        count_launch(3);
+    }
+    return cudaGetLastError();
+}
+
+}  // namespace ss

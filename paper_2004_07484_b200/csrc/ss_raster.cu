@@ -186,7 +186,9 @@ __global__ void __launch_bounds__(TILE_PX) k_raster(RasterArgs a) {
                 if (dist2 < rr && (t > 0.0 || t + sqrt(rr - dist2) > 0.0)) {
                     ++n_hits;
                     const double zz = (far_ - fmin(fmax(zeta, near_), far_)) * inv_range;
-                    const float cl = 1.0f - sqrtf((float)dist2) / rf;
+                    // closeness 1 - dist/r in the cancellation-free form (r^2 - dist^2) / (r (r + dist)):
+                    // near the rim the float32 subtraction would lose all relative accuracy
+                    const float cl = (float)(rr - dist2) / (rf * (rf + sqrtf((float)dist2)));
                     const float o = s_o[j];
                     const float e = (float)((double)o * zz / a.gamma);
                     if (e > m) {  // online form of raster.py:382-387

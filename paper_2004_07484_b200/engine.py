@@ -281,6 +281,8 @@ _engines = {}
 
 
 def default_engine(device="cuda") -> RenderEngine:
+    if not torch.cuda.is_available():
+        raise _lib.NativeLibraryError("CUDA device required: the render path has no CPU fallback")
     dev = torch.device(device)
     if dev.type == "cuda" and dev.index is None:
         dev = torch.device("cuda", torch.cuda.current_device())

@@ -40,8 +40,13 @@ struct TopK {
     int id[KT];
     float c[KT];
     __device__ __forceinline__ void init() {
+        if (KT <= 8) {
 #pragma unroll
-        for (int k = 0; k < KT; ++k) { z[k] = -INFINITY; id[k] = -1; c[k] = 0.0f; }
+            for (int k = 0; k < KT; ++k) { z[k] = -INFINITY; id[k] = -1; c[k] = 0.0f; }
+        } else {  // large K: keep the arrays in (L1-cached) local memory, not 4*KT registers
+#pragma unroll 1
+            for (int k = 0; k < KT; ++k) { z[k] = -INFINITY; id[k] = -1; c[k] = 0.0f; }
+        }
     }
     // keep the KT largest by (z desc, id asc) -- raster.py:389-399
     __device__ __forceinline__ void insert(double zz, int sid, float cl) {
@@ -58,6 +63,7 @@ struct TopK {
                 }
             }
         } else {
+#pragma unroll 1
             for (int k = KT - 1; k > 0; --k) {
                 bool up = z[k] > z[k - 1] || (z[k] == z[k - 1] && id[k] < id[k - 1]);
                 if (!up) break;
@@ -69,21 +75,49 @@ struct TopK {
     }
 };
 
+__device__ __forceinline__ float ex2_approx(float x) {
+    float y;
+    asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+    return y;
+}
+__device__ __forceinline__ float sqrt_approx(float x) {
+    float y;
+    asm("sqrt.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+    return y;
+}
+// keeps a value in a register: stops the compiler from re-deriving it (e.g. re-converting the
+// float64 ray to float32 inside the test loop)
+__device__ __forceinline__ float pin_reg(float x) {
+    asm volatile("" : "+f"(x));
+    return x;
+}
+
+constexpr float kLn2 = 0.6931471805599453f;
+constexpr int QCAP_DRAIN = 5;   // a lane with >= 5 queued hits cannot take a 4-candidate group
+constexpr int DRAIN_MIN_ACTIVE = 12;
+
 template <int DP, int KT, int MODE>
 __global__ void __launch_bounds__(TILE_PX) k_raster(RasterArgs a) {
-    __shared__ float4 s_cf[SS_MAX_CHUNK];  // float centre (or ortho cx, cy), band-widened r^2
-    __shared__ double s_cx[SS_MAX_CHUNK], s_cy[SS_MAX_CHUNK], s_cz[SS_MAX_CHUNK], s_n2[SS_MAX_CHUNK];
-    __shared__ float s_r[SS_MAX_CHUNK], s_o[SS_MAX_CHUNK];
-    __shared__ int s_id[SS_MAX_CHUNK];
-    __shared__ float s_f[SS_MAX_CHUNK * DP];
+    constexpr int CAP = SS_MAX_CHUNK;
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    float4 *s_cf = (float4 *)smem_raw;            // float32 filter: centre (ortho: cx, cy, -), widened r^2
+    float4 *s_misc = s_cf + CAP;                   // r, clamped opacity o, o / gamma * log2(e), sphere id bits
+    double *s_cx = (double *)(s_misc + CAP);       // float64 centre and |c|^2 for the exact decision
+    double *s_cy = s_cx + CAP, *s_cz = s_cy + CAP, *s_n2 = s_cz + CAP;
+    float *s_f = (float *)(s_n2 + CAP);            // features, DP per candidate
     __shared__ double s_red[8];
     __shared__ unsigned long long s_stat[3];
 
     const Cam &cam = a.cam;
     const int tile = blockIdx.x;
     const int tid = threadIdx.x;
-    const int px = (tile % cam.ntx) * TILE + (tid & (TILE - 1));
-    const int py = (tile / cam.ntx) * TILE + (tid >> 4);
+    const int lane = tid & 31, warp = tid >> 5;
+    // each warp owns an 8x4 pixel block of the 16x16 tile (2 x 4 blocks): a sphere footprint
+    // touches fewer warps than with 16x2 strips, and a warp row is one 32-byte sector
+    const int lx = ((warp & 1) << 3) | (lane & 7);
+    const int ly = ((warp >> 1) << 2) | (lane >> 3);
+    const int px = (tile % cam.ntx) * TILE + lx;
+    const int py = (tile / cam.ntx) * TILE + ly;
     const bool valid = px < cam.W && py < cam.H;
 
     // pixel-centre ray, camera frame (camera.py:332-357)
@@ -94,8 +128,12 @@ __global__ void __launch_bounds__(TILE_PX) k_raster(RasterArgs a) {
         double vn = sqrt(xs * xs + ys * ys + cam.focal * cam.focal);
         ux = xs / vn; uy = ys / vn; uz = cam.focal / vn;
     }
-    const float uxf = (float)ux, uyf = (float)uy, uzf = (float)uz;
-    const float xsf = (float)xs, ysf = (float)ys;
+    // float32 copies for the filter; an out-of-image pixel gets a NaN ray so it never passes
+    float fx = (MODE == SS_MODE_PINHOLE) ? (float)ux : (float)xs;
+    float fy = (MODE == SS_MODE_PINHOLE) ? (float)uy : (float)ys;
+    float fz = (float)uz;
+    if (!valid) fx = __int_as_float(0x7fc00000);
+    fx = pin_reg(fx); fy = pin_reg(fy); fz = pin_reg(fz);
 
     const bool overflow = (a.status[ST_FLAGS] & SS_FLAG_PAIR_OVERFLOW) != 0;  // lists not built
     const int s0 = a.tile_start[tile];
@@ -106,7 +144,7 @@ __global__ void __launch_bounds__(TILE_PX) k_raster(RasterArgs a) {
     if (a.tau_on && MODE == SS_MODE_PINHOLE && n_cand > 0) {
         double v = valid ? uz : INFINITY;
         for (int o = 16; o > 0; o >>= 1) v = fmin(v, __shfl_xor_sync(0xffffffffu, v, o));
-        if ((tid & 31) == 0) s_red[tid >> 5] = v;
+        if (lane == 0) s_red[warp] = v;
         __syncthreads();
         v = s_red[0];
 #pragma unroll
@@ -115,7 +153,9 @@ __global__ void __launch_bounds__(TILE_PX) k_raster(RasterArgs a) {
     }
     if (tid < 3) s_stat[tid] = 0;
 
-    float m = (float)a.eps_over_g, denom = 1.0f;
+    // blend state in base-2 exponent units: mass = o c 2^(e2), e2 = o z / gamma * log2(e)
+    const float m2_bg = (float)(a.eps_over_g * 1.4426950408889634);
+    float m2 = m2_bg, denom = 1.0f;
     float num[DP];
 #pragma unroll
     for (int i = 0; i < DP; ++i) num[i] = 0.0f;
@@ -125,18 +165,66 @@ __global__ void __launch_bounds__(TILE_PX) k_raster(RasterArgs a) {
     unsigned n_hits = 0;
     long long scanned = 0;
     const double near_ = cam.near_, far_ = cam.far_, inv_range = cam.inv_range;
+    const float inv_g2 = (float)(1.4426950408889634 / a.gamma);
+
+    // exact hit evaluation for one queued candidate (reference raster.py:307-324, :380-399)
+    auto process = [&](int j) {
+        double t, dist2, zeta;
+        if (MODE == SS_MODE_PINHOLE) {
+            t = ux * s_cx[j] + uy * s_cy[j] + uz * s_cz[j];
+            dist2 = s_n2[j] - t * t;
+            dist2 = dist2 < 0.0 ? 0.0 : dist2;
+            zeta = t * uz;
+        } else {
+            t = s_cz[j];
+            const double dx = s_cx[j] - xs, dy = s_cy[j] - ys;
+            dist2 = dx * dx + dy * dy;
+            zeta = t;
+        }
+        const float4 mi = s_misc[j];
+        const float rf = mi.x;
+        const double rr = (double)rf * (double)rf;
+        const double hc2 = rr - dist2;
+        if (!(hc2 > 0.0)) return;                        // dist2 < r^2
+        if (!(t > 0.0) && !(t + sqrt(hc2) > 0.0)) return;  // t + half_chord > 0
+        ++n_hits;
+        double zc = zeta < near_ ? near_ : zeta;
+        zc = zc > far_ ? far_ : zc;
+        const double zz = (far_ - zc) * inv_range;
+        // closeness 1 - dist/r as (r^2 - dist^2) / (r (r + dist)): no cancellation near the rim
+        const float cl = __fdividef((float)hc2, rf * (rf + sqrt_approx((float)dist2)));
+        const float e2 = (float)zz * mi.z;
+        if (e2 > m2) {  // online form of raster.py:382-387
+            const float sc = ex2_approx(m2 - e2);
+            denom *= sc;
+#pragma unroll
+            for (int i = 0; i < DP; ++i) num[i] *= sc;
+            m2 = e2;
+        }
+        const float oc = mi.y * cl;
+        const float x2 = e2 - m2;
+        const float term = oc * ex2_approx(x2);
+        denom += term;
+#pragma unroll
+        for (int i = 0; i < DP; ++i) num[i] = fmaf(term, s_f[j * DP + i], num[i]);
+        // store rule term > 0 (raster.py:389) as the float64 reference sees it: float32 (FTZ)
+        // underflows ~950 binary orders earlier than float64, so re-derive it in the log domain
+        bool store = term > 0.0f;
+        if (!store && oc > 0.0f) store = x2 + log2f(oc) > -1075.0f;
+        if (store) top.insert(zz, __float_as_int(mi.w), cl);
+    };
 
     for (int start = 0; start < n_cand; start += a.chunk) {
         const int cn = min(a.chunk, n_cand - start);
+        const int cn4 = (cn + 3) & ~3;
         __syncthreads();  // previous batch fully consumed
         if (tid < cn) {
             const int sid = a.pair_id[s0 + start + tid];
             const Rec rc = a.rec[sid];
             const double n2 = rc.cx * rc.cx + rc.cy * rc.cy + rc.cz * rc.cz;
             s_cx[tid] = rc.cx; s_cy[tid] = rc.cy; s_cz[tid] = rc.cz; s_n2[tid] = n2;
-            s_r[tid] = rc.r; s_o[tid] = rc.o; s_id[tid] = sid;
-            // float32 filter radius: r + delta with delta >= the worst-case error of the
-            // float32 distance, rounded up.
+            s_misc[tid] = make_float4(rc.r, rc.o, rc.o * inv_g2, __int_as_float(sid));
+            // float32 filter radius r + delta, delta >= worst-case error of the float32 distance
             float cn32 = (MODE == SS_MODE_PINHOLE)
                              ? (float)sqrt(n2)
                              : fabsf((float)rc.cx) + fabsf((float)rc.cy) + (float)(cam.sensor_w);
@@ -145,72 +233,53 @@ __global__ void __launch_bounds__(TILE_PX) k_raster(RasterArgs a) {
             const float *f = a.feat + (size_t)sid * a.d;
 #pragma unroll
             for (int i = 0; i < DP; ++i) s_f[tid * DP + i] = i < a.d ? f[i] : 0.0f;
+        } else if (tid < cn4) {
+            s_cf[tid] = make_float4(0.f, 0.f, 0.f, -1.0f);  // padding: never passes the filter
         }
         __syncthreads();
         if (a.tau_on) {  // vote, raster.py:364-368
-            const double e0 = (MODE == SS_MODE_PINHOLE) ? sqrt(s_n2[0]) - (double)s_r[0]
-                                                       : s_cz[0] - (double)s_r[0];
+            const double e0 = (MODE == SS_MODE_PINHOLE) ? sqrt(s_n2[0]) - (double)s_misc[0].x
+                                                       : s_cz[0] - (double)s_misc[0].x;
             const double zb = (far_ - fmin(fmax(e0 * tile_cos, near_), far_)) * inv_range;
-            const double z_stop = a.gamma * (a.log_tau + (double)m + (double)logf(denom));
-            done = done || (zb < z_stop);
+            const double z_stop = a.gamma * (a.log_tau + (double)((m2 + log2f(denom)) * kLn2));
+            if (!done && zb < z_stop) {
+                done = true;
+                fx = pin_reg(__int_as_float(0x7fc00000));  // a finished pixel ignores later hits (:375-376)
+            }
             if (__syncthreads_and(done)) break;
         }
         scanned += cn;
-        if (done) continue;
-        for (int j = 0; j < cn; ++j) {
-            const float4 c = s_cf[j];
-            float d2;
-            if (MODE == SS_MODE_PINHOLE) {
-                const float t = fmaf(uxf, c.x, fmaf(uyf, c.y, uzf * c.z));
-                const float dx = fmaf(-t, uxf, c.x), dy = fmaf(-t, uyf, c.y), dz = fmaf(-t, uzf, c.z);
-                d2 = fmaf(dx, dx, fmaf(dy, dy, dz * dz));
-            } else {
-                const float dx = c.x - xsf, dy = c.y - ysf;
-                d2 = fmaf(dx, dx, dy * dy);
-            }
-            if (d2 < c.w) {
-                // exact decision with the reference's float64 formula (raster.py:307-324)
-                double t, dist2, zeta;
+        if (__all_sync(0xffffffffu, done)) continue;  // warp-uniform
+
+        // float32 filter over the batch; candidates that pass go to a per-lane FIFO (8 x 8 bit)
+        // that the whole warp drains together, so the float64 path runs with most lanes active
+        unsigned long long q = 0;
+        int qn = 0;
+        for (int j0 = 0; j0 < cn4; j0 += 4) {
+#pragma unroll
+            for (int u = 0; u < 4; ++u) {
+                const float4 c = s_cf[j0 + u];
+                float d2;
                 if (MODE == SS_MODE_PINHOLE) {
-                    t = ux * s_cx[j] + uy * s_cy[j] + uz * s_cz[j];
-                    dist2 = fmax(s_n2[j] - t * t, 0.0);
-                    zeta = t * uz;
+                    const float t = fmaf(fx, c.x, fmaf(fy, c.y, fz * c.z));
+                    const float dx = fmaf(-t, fx, c.x), dy = fmaf(-t, fy, c.y), dz = fmaf(-t, fz, c.z);
+                    d2 = fmaf(dx, dx, fmaf(dy, dy, dz * dz));
                 } else {
-                    t = s_cz[j];
-                    const double dx = s_cx[j] - xs, dy = s_cy[j] - ys;
-                    dist2 = dx * dx + dy * dy;
-                    zeta = t;
+                    const float dx = c.x - fx, dy = c.y - fy;
+                    d2 = fmaf(dx, dx, dy * dy);
                 }
-                const float rf = s_r[j];
-                const double rr = (double)rf * (double)rf;
-                if (dist2 < rr && (t > 0.0 || t + sqrt(rr - dist2) > 0.0)) {
-                    ++n_hits;
-                    const double zz = (far_ - fmin(fmax(zeta, near_), far_)) * inv_range;
-                    // closeness 1 - dist/r in the cancellation-free form (r^2 - dist^2) / (r (r + dist)):
-                    // near the rim the float32 subtraction would lose all relative accuracy
-                    const float cl = (float)(rr - dist2) / (rf * (rf + sqrtf((float)dist2)));
-                    const float o = s_o[j];
-                    const float e = (float)((double)o * zz / a.gamma);
-                    if (e > m) {  // online form of raster.py:382-387
-                        const float sc = expf(m - e);
-                        denom *= sc;
-#pragma unroll
-                        for (int i = 0; i < DP; ++i) num[i] *= sc;
-                        m = e;
-                    }
-                    const float oc = o * cl;
-                    const float x = e - m;
-                    const float term = oc * expf(x);
-                    denom += term;
-#pragma unroll
-                    for (int i = 0; i < DP; ++i) num[i] = fmaf(term, s_f[j * DP + i], num[i]);
-                    // store rule term > 0 (raster.py:389) evaluated as the float64 reference
-                    // would: float32 underflows ~640 units of exponent earlier.
-                    bool store = term > 0.0f;
-                    if (!store && oc > 0.0f) store = x + logf(oc) > -745.13f;
-                    if (store) top.insert(zz, s_id[j], cl);
+                if (d2 < c.w) { q = (q << 8) | (unsigned)(j0 + u); ++qn; }
+            }
+            if (__any_sync(0xffffffffu, qn >= QCAP_DRAIN)) {
+                while (true) {
+                    const unsigned act = __ballot_sync(0xffffffffu, qn > 0);
+                    if (__popc(act) < DRAIN_MIN_ACTIVE && !__any_sync(0xffffffffu, qn >= QCAP_DRAIN)) break;
+                    if (qn > 0) { --qn; process((int)((q >> (8 * qn)) & 0xffull)); }
                 }
             }
+        }
+        while (__any_sync(0xffffffffu, qn > 0)) {
+            if (qn > 0) { --qn; process((int)((q >> (8 * qn)) & 0xffull)); }
         }
     }
 
@@ -218,24 +287,34 @@ __global__ void __launch_bounds__(TILE_PX) k_raster(RasterArgs a) {
     if (valid) {
         const size_t P = (size_t)cam.W * cam.H;
         const size_t pix = (size_t)py * cam.W + px;
-        const float ld = m + logf(denom);
-        const float w_bg = expf((float)a.eps_over_g - ld);
+        const float ld2 = m2 + log2f(denom);
+        const float w_bg = exp2f(m2_bg - ld2);
         const float inv = 1.0f / denom;
 #pragma unroll
         for (int i = 0; i < DP; ++i)
             if (i < a.d) a.image[pix * a.d + i] = fmaf(w_bg, a.bg[i], num[i] * inv);
         a.bg_weight[pix] = w_bg;
         if (a.store_buffer) {
+            if (KT <= 8) {
 #pragma unroll
-            for (int k = 0; k < KT; ++k) {
-                if (k < a.K) {
+                for (int k = 0; k < KT; ++k) {
+                    if (k < a.K) {
+                        const bool empty = top.id[k] < 0;
+                        a.ids[k * P + pix] = top.id[k];
+                        a.z[k * P + pix] = empty ? 0.0f : (float)top.z[k];
+                        a.clos[k * P + pix] = top.c[k];
+                    }
+                }
+            } else {
+#pragma unroll 1
+                for (int k = 0; k < a.K; ++k) {
                     const bool empty = top.id[k] < 0;
                     a.ids[k * P + pix] = top.id[k];
                     a.z[k * P + pix] = empty ? 0.0f : (float)top.z[k];
                     a.clos[k * P + pix] = top.c[k];
                 }
             }
-            a.log_denom[pix] = ld;
+            a.log_denom[pix] = ld2 * kLn2;
         }
     }
     if (a.collect_stats) {
@@ -246,7 +325,7 @@ __global__ void __launch_bounds__(TILE_PX) k_raster(RasterArgs a) {
             st += __shfl_xor_sync(0xffffffffu, st, o);
         }
         __syncthreads();
-        if ((tid & 31) == 0) {
+        if (lane == 0) {
             atomicAdd(&s_stat[1], (unsigned long long)h);
             atomicAdd(&s_stat[2], (unsigned long long)st);
         }
@@ -259,10 +338,25 @@ __global__ void __launch_bounds__(TILE_PX) k_raster(RasterArgs a) {
     }
 }
 
+template <int DP>
+constexpr size_t raster_smem_bytes() { return (size_t)SS_MAX_CHUNK * (16 + 16 + 32 + 4 * DP); }
+
+template <int DP, int KT, int MODE>
+void launch_one(const RasterArgs &r, int n_tiles, cudaStream_t s) {
+    constexpr size_t smem = raster_smem_bytes<DP>();
+    static bool attr_done = false;  // per instantiation
+    if (!attr_done) {
+        if (smem + 1024 > 48 * 1024)
+            cudaFuncSetAttribute(k_raster<DP, KT, MODE>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        attr_done = true;
+    }
+    k_raster<DP, KT, MODE><<<n_tiles, TILE_PX, smem, s>>>(r);
+}
+
 template <int DP, int KT>
 void launch_mode(const RasterArgs &r, int n_tiles, int mode, cudaStream_t s) {
-    if (mode == SS_MODE_PINHOLE) k_raster<DP, KT, SS_MODE_PINHOLE><<<n_tiles, TILE_PX, 0, s>>>(r);
-    else k_raster<DP, KT, SS_MODE_ORTHOGRAPHIC><<<n_tiles, TILE_PX, 0, s>>>(r);
+    if (mode == SS_MODE_PINHOLE) launch_one<DP, KT, SS_MODE_PINHOLE>(r, n_tiles, s);
+    else launch_one<DP, KT, SS_MODE_ORTHOGRAPHIC>(r, n_tiles, s);
 }
 
 template <int DP>

@@ -117,10 +117,11 @@ def test_gating_and_normalisation_rules(engine):
     gated = pr <= 3.0
     assert gated.any() and (~gated & (cnt > 0)).any()
     div = np.maximum(cnt, 1)[:, None]
-    assert_close(nrm["d_feat"].cpu().numpy(), raw["d_feat"].cpu().numpy() / div, 1e-5, 1e-9, "d_feature / count")
+    # two launches sum their float32 atomics in different orders: compare to atomics tolerance
+    grad_close(nrm["d_feat"].cpu().numpy(), raw["d_feat"].cpu().numpy() / div, "d_feature / count", rtol=2e-5)
     dp = nrm["d_pos"].cpu().numpy()
     assert np.all(dp[gated] == 0) and np.all(nrm["d_rad"].cpu().numpy()[gated] == 0)
-    assert_close(dp[~gated], (raw["d_pos"].cpu().numpy() / div)[~gated], 1e-5, 1e-9, "d_position / count")
+    grad_close(dp[~gated], (raw["d_pos"].cpu().numpy() / div)[~gated], "d_position / count", rtol=2e-5)
     ocam = orc.camera_from_vector(vec, 64, 64)
     ref = orc.render_forward(pos, rad, opa, feat, bg, ocam, gamma=0.1, tau=0.0)
     gr = orc.render_backward(pos, rad, opa, feat, bg, ocam, ref, up.astype(np.float64))
@@ -134,7 +135,7 @@ def test_early_stop_bound_and_chunk_sizes(engine, chunk):
     from oracle import oracle as orc
     from paper_2004_07484_b200 import CameraSpec, camera_from_vector
     from paper_2004_07484_b200.synthetic import benchmark_scene
-    pos, rad, opa, feat, bg, vec = benchmark_scene(3000, 96, 96, seed=2, profile="occluded")
+    pos, rad, opa, feat, bg, vec = benchmark_scene(20000, 96, 96, seed=2, profile="occluded")
     spec = CameraSpec.from_camera(camera_from_vector(vec, 96, 96))
     ocam = orc.camera_from_vector(vec, 96, 96)
     f0 = engine.forward(pos, rad, opa, feat, bg, spec, gamma=0.1, tau=0.0, top_k=5, chunk=chunk, collect_stats=True)
@@ -183,13 +184,13 @@ def test_long_tile_lists_use_the_big_sort_paths(engine):
         opa = rng.uniform(0.2, 1.0, m).astype(np.float32)
         feat = rng.uniform(0, 1, (m, 3)).astype(np.float32)
         bg = np.zeros(3, np.float32)
-        spec = CameraSpec.from_camera(camera_from_vector(vec, 32, 32))
+        spec = CameraSpec.from_camera(camera_from_vector(vec, 16, 16))
         f = engine.forward(pos, rad, opa, feat, bg, spec, gamma=0.1, tau=0.0, collect_stats=True)
-        starts, ids = engine.tile_lists(m, 3, 32, 32, 5)
-        o_ids, o_starts = orc.tile_lists(pos, rad, orc.camera_from_vector(vec, 32, 32))
+        starts, ids = engine.tile_lists(m, 3, 16, 16, 5)
+        o_ids, o_starts = orc.tile_lists(pos, rad, orc.camera_from_vector(vec, 16, 16))
         assert int(np.diff(o_starts).max()) > (2048 if m == 3000 else 8192)
         assert np.array_equal(starts, o_starts) and np.array_equal(ids, o_ids)
-        ref = orc.render_forward(pos, rad, opa, feat, bg, orc.camera_from_vector(vec, 32, 32), gamma=0.1, tau=0.0)
+        ref = orc.render_forward(pos, rad, opa, feat, bg, orc.camera_from_vector(vec, 16, 16), gamma=0.1, tau=0.0)
         assert np.array_equal(f["ids"].permute(1, 2, 0).cpu().numpy(), ref["ids"])
 
 

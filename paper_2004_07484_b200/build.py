@@ -62,4 +62,5 @@ def build(force: bool = False, verbose: bool = False, extra_flags=()) -> str:
 
 if __name__ == "__main__":
     v = "-v" in sys.argv
-    print(build(force=True, verbose=v, extra_flags=("-Xptxas", "-v") if v else ()))
+    extra = [a for a in sys.argv[1:] if a.startswith("-D")]
+    print(build(force=True, verbose=v, extra_flags=tuple(extra) + (("-Xptxas", "-v") if v else ())))

@@ -6,11 +6,13 @@
 // read in the test loop is a broadcast.
 //
 // Precision plan: the float64 reference decides hits with
-// dist^2 = |c|^2 - t^2 and orders the per-pixel top-K by float64 NDC depth.  Here a float32
-// test in the cancellation-free form d = c - t u, widened by a rigorous error band, filters
-// candidates; every candidate that passes is re-evaluated with the reference's own float64
-// formula, which alone decides hit / miss and produces the depth used for ordering.  The
-// blend (online softmax of Eq. 1) runs in float32.
+// dist^2 = |c|^2 - t^2 and orders the per-pixel top-K by float64 NDC depth.  Here a cheap
+// float32 screen-space test filters candidates: a pixel can only hit a sphere if it lies inside
+// the circle, centred on the projected sphere centre, that bounds the sphere's projected
+// outline (radius f (tan(theta + alpha) - tan(theta)), widened for float32 rounding).  Every
+// candidate that passes is re-evaluated with the reference's own float64 formula, which alone
+// decides hit / miss and produces the depth used for ordering.  The blend (online softmax of
+// Eq. 1) runs in float32.
 #include <math.h>
 
 #include "ss_common.cuh"
@@ -93,11 +95,13 @@ __device__ __forceinline__ float pin_reg(float x) {
 }
 
 constexpr float kLn2 = 0.6931471805599453f;
-constexpr int QCAP_DRAIN = 5;   // a lane with >= 5 queued hits cannot take a 4-candidate group
+#ifndef SS_RASTER_MINB
+#define SS_RASTER_MINB 3  // resident CTAs per SM the register allocation targets (d <= 4, K <= 8)
+#endif
 constexpr int DRAIN_MIN_ACTIVE = 12;
 
 template <int DP, int KT, int MODE>
-__global__ void __launch_bounds__(TILE_PX) k_raster(RasterArgs a) {
+__global__ void __launch_bounds__(TILE_PX, (KT <= 8 && DP <= 4) ? SS_RASTER_MINB : 1) k_raster(RasterArgs a) {
     constexpr int CAP = SS_MAX_CHUNK;
     extern __shared__ __align__(16) unsigned char smem_raw[];
     float4 *s_cf = (float4 *)smem_raw;            // float32 filter: centre (ortho: cx, cy, -), widened r^2
@@ -128,12 +132,12 @@ __global__ void __launch_bounds__(TILE_PX) k_raster(RasterArgs a) {
         double vn = sqrt(xs * xs + ys * ys + cam.focal * cam.focal);
         ux = xs / vn; uy = ys / vn; uz = cam.focal / vn;
     }
-    // float32 copies for the filter; an out-of-image pixel gets a NaN ray so it never passes
-    float fx = (MODE == SS_MODE_PINHOLE) ? (float)ux : (float)xs;
-    float fy = (MODE == SS_MODE_PINHOLE) ? (float)uy : (float)ys;
-    float fz = (float)uz;
-    if (!valid) fx = __int_as_float(0x7fc00000);
-    fx = pin_reg(fx); fy = pin_reg(fy); fz = pin_reg(fz);
+    // float32 sensor coordinates for the screen-space filter; an out-of-image (or finished) pixel
+    // is moved far away so it never passes
+    constexpr float kFar = 1e30f;
+    float fx = valid ? (float)xs : kFar;
+    float fy = (float)ys;
+    fx = pin_reg(fx); fy = pin_reg(fy);
 
     const bool overflow = (a.status[ST_FLAGS] & SS_FLAG_PAIR_OVERFLOW) != 0;  // lists not built
     const int s0 = a.tile_start[tile];
@@ -224,17 +228,32 @@ __global__ void __launch_bounds__(TILE_PX) k_raster(RasterArgs a) {
             const double n2 = rc.cx * rc.cx + rc.cy * rc.cy + rc.cz * rc.cz;
             s_cx[tid] = rc.cx; s_cy[tid] = rc.cy; s_cz[tid] = rc.cz; s_n2[tid] = n2;
             s_misc[tid] = make_float4(rc.r, rc.o, rc.o * inv_g2, __int_as_float(sid));
-            // float32 filter radius r + delta, delta >= worst-case error of the float32 distance
-            float cn32 = (MODE == SS_MODE_PINHOLE)
-                             ? (float)sqrt(n2)
-                             : fabsf((float)rc.cx) + fabsf((float)rc.cy) + (float)(cam.sensor_w);
-            float rb = rc.r + 1e-6f * (cn32 + rc.r);
-            s_cf[tid] = make_float4((float)rc.cx, (float)rc.cy, (float)rc.cz, rb * rb * 1.000001f);
+            // screen-space filter record: projected centre and bounding-circle radius (float64
+            // here, once per candidate; float32 + rounding pad in the test loop)
+            double pcx, pcy, rho;
+            if (MODE == SS_MODE_PINHOLE) {
+                const double rr = (double)rc.r * (double)rc.r;
+                rho = INFINITY; pcx = 0.0; pcy = 0.0;  // default: always passes (camera near/inside the sphere)
+                if (rc.cz > (double)rc.r && n2 > rr) {
+                    const double tan_t = sqrt(rc.cx * rc.cx + rc.cy * rc.cy) / rc.cz;
+                    const double tan_a = (double)rc.r / sqrt(n2 - rr);
+                    const double den = 1.0 - tan_t * tan_a;
+                    if (den > 1e-6) {
+                        rho = cam.focal * ((tan_t + tan_a) / den - tan_t);
+                        pcx = cam.focal * rc.cx / rc.cz;
+                        pcy = cam.focal * rc.cy / rc.cz;
+                    }
+                }
+            } else {
+                pcx = rc.cx; pcy = rc.cy; rho = (double)rc.r;
+            }
+            const float rho_pad = (float)(rho * (1.0 + 1e-5) + 4e-7 * (fabs(pcx) + fabs(pcy) + cam.sensor_w));
+            s_cf[tid] = make_float4((float)pcx, (float)pcy, rho_pad * rho_pad * 1.000001f, 0.0f);
             const float *f = a.feat + (size_t)sid * a.d;
 #pragma unroll
             for (int i = 0; i < DP; ++i) s_f[tid * DP + i] = i < a.d ? f[i] : 0.0f;
         } else if (tid < cn4) {
-            s_cf[tid] = make_float4(0.f, 0.f, 0.f, -1.0f);  // padding: never passes the filter
+            s_cf[tid] = make_float4(0.f, 0.f, -1.0f, 0.f);  // padding: never passes the filter
         }
         __syncthreads();
         if (a.tau_on) {  // vote, raster.py:364-368
@@ -244,43 +263,49 @@ __global__ void __launch_bounds__(TILE_PX) k_raster(RasterArgs a) {
             const double z_stop = a.gamma * (a.log_tau + (double)((m2 + log2f(denom)) * kLn2));
             if (!done && zb < z_stop) {
                 done = true;
-                fx = pin_reg(__int_as_float(0x7fc00000));  // a finished pixel ignores later hits (:375-376)
+                fx = pin_reg(kFar);  // a finished pixel ignores later hits (raster.py:375-376)
             }
             if (__syncthreads_and(done)) break;
         }
         scanned += cn;
         if (__all_sync(0xffffffffu, done)) continue;  // warp-uniform
 
-        // float32 filter over the batch; candidates that pass go to a per-lane FIFO (8 x 8 bit)
-        // that the whole warp drains together, so the float64 path runs with most lanes active
+        // float32 filter over the batch, 4 candidates per step.  The sign bits of (d^2 - rho^2) are
+        // funnel-shifted into a 4-bit mask; a non-empty mask is pushed as one 10-bit entry
+        // [group:6 | mask:4] into a per-lane FIFO (6 entries in 64 bits).  The warp drains the
+        // FIFOs together, so the float64 path below runs with most lanes active.
         unsigned long long q = 0;
         int qn = 0;
+        unsigned cur = 0;  // entry being consumed
+        auto drain_round = [&]() {
+            if ((cur & 15u) == 0u && qn > 0) { --qn; cur = (unsigned)(q >> (10 * qn)) & 0x3ffu; }
+            if (cur & 15u) {
+                const int bit = 31 - __clz((int)(cur & 15u));  // candidate u sits at bit 3 - u
+                const int j = (int)((cur >> 4) << 2) + (3 - bit);
+                cur &= ~(1u << bit);
+                process(j);
+            }
+        };
         for (int j0 = 0; j0 < cn4; j0 += 4) {
+            unsigned acc = 0;
 #pragma unroll
             for (int u = 0; u < 4; ++u) {
                 const float4 c = s_cf[j0 + u];
-                float d2;
-                if (MODE == SS_MODE_PINHOLE) {
-                    const float t = fmaf(fx, c.x, fmaf(fy, c.y, fz * c.z));
-                    const float dx = fmaf(-t, fx, c.x), dy = fmaf(-t, fy, c.y), dz = fmaf(-t, fz, c.z);
-                    d2 = fmaf(dx, dx, fmaf(dy, dy, dz * dz));
-                } else {
-                    const float dx = c.x - fx, dy = c.y - fy;
-                    d2 = fmaf(dx, dx, dy * dy);
-                }
-                if (d2 < c.w) { q = (q << 8) | (unsigned)(j0 + u); ++qn; }
+                const float dx = fx - c.x, dy = fy - c.y;
+                const float sgn = fmaf(dx, dx, dy * dy) - c.z;  // negative = inside the bounding circle
+                acc = __funnelshift_l(__float_as_uint(sgn), acc, 1);
             }
-            if (__any_sync(0xffffffffu, qn >= QCAP_DRAIN)) {
+            acc &= 15u;
+            if (acc) { q = (q << 10) | (unsigned long long)(((unsigned)j0 << 2) | acc); ++qn; }
+            if (__any_sync(0xffffffffu, qn >= 6)) {
                 while (true) {
-                    const unsigned act = __ballot_sync(0xffffffffu, qn > 0);
-                    if (__popc(act) < DRAIN_MIN_ACTIVE && !__any_sync(0xffffffffu, qn >= QCAP_DRAIN)) break;
-                    if (qn > 0) { --qn; process((int)((q >> (8 * qn)) & 0xffull)); }
+                    const unsigned act = __ballot_sync(0xffffffffu, qn > 0 || (cur & 15u));
+                    if (__popc(act) < DRAIN_MIN_ACTIVE && !__any_sync(0xffffffffu, qn >= 6)) break;
+                    drain_round();
                 }
             }
         }
-        while (__any_sync(0xffffffffu, qn > 0)) {
-            if (qn > 0) { --qn; process((int)((q >> (8 * qn)) & 0xffull)); }
-        }
+        while (__any_sync(0xffffffffu, qn > 0 || (cur & 15u))) drain_round();
     }
 
     // finalise, raster.py:401-414

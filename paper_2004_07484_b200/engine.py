@@ -244,7 +244,7 @@ class RenderEngine:
                    "pixel_count": torch.empty((m,), dtype=torch.int32, device=dev)}
             accumulate = False
         if camera_grads and "cam_grad" not in out:
-            out["cam_grad"] = torch.zeros(16, dtype=torch.float64, device=dev)
+            out["cam_grad"] = torch.empty(16, dtype=torch.float64, device=dev)  # fully written by the kernels
         fwd_key = (m, d, w, h, k, pos.data_ptr(), tuple(np.asarray(cam.t).tolist()),
                    tuple(np.asarray(cam.R).reshape(-1).tolist()), cam.focal, cam.sensor_w, cam.mode)
         reuse = self._ws is not None and self._last_fwd_key == fwd_key

@@ -71,10 +71,12 @@ class ViewShardedRenderer:
         Fills `grads` with the sum over ALL views (after the allreduce) and returns
         {view: cam_grad tensor} for the local views."""
         pos, rad, opa, feat, bg = scene
-        grads.zero_()
         cam_out = {}
         out = grads.as_out()
-        for v in self.local_views(len(cameras)):
+        local = self.local_views(len(cameras))
+        if not local:
+            grads.zero_()
+        for i, v in enumerate(local):
             cam = cameras[v]
             f = self.engine.forward(pos, rad, opa, feat, bg, cam, gamma=gamma, eps=eps, tau=tau, top_k=top_k,
                                     check=check)
@@ -82,7 +84,7 @@ class ViewShardedRenderer:
             o = dict(out)
             res = self.engine.backward(pos, rad, opa, feat, bg, cam, f, up, gamma=gamma, eps=eps,
                                        normalize=normalize, gate=gate, camera_grads=camera_grads, out=o,
-                                       accumulate=True)
+                                       accumulate=(i > 0))  # the first local view overwrites: no zero fill
             if camera_grads:
                 cam_out[v] = res["cam_grad"]
         if self.world_size > 1:

@@ -27,7 +27,9 @@ class OracleEngine:
                  out, accumulate):
         g = orc.render_backward(pos.numpy(), rad.numpy(), opa.numpy(), feat.numpy(), bg.numpy(), cam, buf,
                                 upstream.numpy().astype(np.float64), normalize=normalize, gate=gate)
-        assert accumulate
+        if not accumulate:
+            for k in ("d_pos", "d_rad", "d_opa", "d_feat", "pixel_count"):
+                out[k].zero_()
         out["d_pos"] += torch.from_numpy(g["d_position"]).float()
         out["d_rad"] += torch.from_numpy(g["d_radius"]).float()
         out["d_opa"] += torch.from_numpy(g["d_opacity"]).float()

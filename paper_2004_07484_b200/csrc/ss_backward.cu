@@ -29,25 +29,127 @@ struct BackArgs {
 };
 
 __device__ __forceinline__ void red_add_v4(float *addr, float a, float b, float c, float d) {
+#ifdef SS_EXPERIMENT_NO_RED  // measurement only: floor of the kernel without the reductions
+    if (a == 123456.f) *addr = b + c + d;
+    return;
+#endif
     asm volatile("red.global.add.v4.f32 [%0], {%1, %2, %3, %4};" ::"l"(addr), "f"(a), "f"(b), "f"(c), "f"(d)
                  : "memory");
 }
 
+// Per-hit gradient pieces for one stored slot (grad.py:110-179); accumulates into the sphere's row.
 template <int DP, int MODE>
-__global__ void __launch_bounds__(TILE_PX) k_backward(BackArgs a) {
+__device__ __forceinline__ void slot_gradient(const BackArgs &a, const Rec &rc, int id, float zk, float ck,
+                                              float ld, float inv_g, const float *up, const float *fhat,
+                                              const float *f, int d, double xs, double ys, double ux, double uy,
+                                              double uz, double inv_vnorm) {
+    const Cam &cam = a.cam;
+    const float o = rc.o;
+    const float ez = o * zk * inv_g;
+    const float E = expf(ez - ld);
+    const float w = o * ck * E;
+    float acoef = 0.0f;
+#pragma unroll
+    for (int i = 0; i < DP; ++i)
+        if (i < d) acoef = fmaf(up[i], f[i] - fhat[i], acoef);
+    const float dl_dz = acoef * w * o * inv_g;
+    const float dl_dc = acoef * o * E;
+    const float dl_do = acoef * ck * E * (1.0f + ez);
+
+    // geometry chain (grad.py:117-165).  Only the cancelling part -- t = c.u and d = c - t u with
+    // |c| ~ 1e3 |d| -- is float64; everything downstream is float32 on well-conditioned values.
+    const float r = rc.r;
+    float t, dvx, dvy, dvz, dist;
+    if (MODE == SS_MODE_PINHOLE) {
+        const double td = rc.cx * ux + rc.cy * uy + rc.cz * uz;
+        const double ddx = rc.cx - td * ux, ddy = rc.cy - td * uy, ddz = rc.cz - td * uz;
+        t = (float)td; dvx = (float)ddx; dvy = (float)ddy; dvz = (float)ddz;
+        dist = sqrtf((float)(ddx * ddx + ddy * ddy + ddz * ddz));
+    } else {
+        const double ddx = rc.cx - xs, ddy = rc.cy - ys;
+        t = (float)rc.cz; dvx = (float)ddx; dvy = (float)ddy; dvz = 0.0f;
+        dist = sqrtf((float)(ddx * ddx + ddy * ddy));
+    }
+    const bool interior = (0.0f < zk) && (zk < 1.0f);
+    const float dl_dzeta = interior ? -dl_dz * (float)cam.inv_range : 0.0f;
+    const float inv_r = 1.0f / r;
+    const float dl_ddist = -dl_dc * inv_r;
+    const float d_radius = dl_dc * dist * inv_r * inv_r;
+    const float inv_dist = dist > 1e-12f ? 1.0f / dist : 0.0f;
+    const float hx = dvx * inv_dist, hy = dvy * inv_dist, hz = dvz * inv_dist;
+    const float xsf = (float)xs, ysf = (float)ys;
+    float gcx, gcy, gcz, g_focal, g_sensor;
+    if (MODE == SS_MODE_PINHOLE) {
+        const float uxf = (float)ux, uyf = (float)uy, uzf = (float)uz;
+        const float zu = dl_dzeta * uzf;
+        gcx = fmaf(dl_ddist, hx, zu * uxf);
+        gcy = fmaf(dl_ddist, hy, zu * uyf);
+        gcz = fmaf(dl_ddist, hz, zu * uzf);
+        // intrinsics chain (grad.py:141-154): grad_u = s1 c + dl_dzeta t e_z projected off u.  With
+        // c = t u + d the projection is s1 d + dl_dzeta t (e_z - u_z u): same value, no cancellation.
+        const float s1 = fmaf(-dl_ddist * t, inv_dist, zu);
+        const float zt = dl_dzeta * t;
+        const float prx = fmaf(s1, dvx, -zt * uzf * uxf);
+        const float pry = fmaf(s1, dvy, -zt * uzf * uyf);
+        const float prz = fmaf(s1, dvz, zt * (1.0f - uzf * uzf));
+        const float ivn = (float)inv_vnorm;
+        g_focal = prz * ivn;
+        g_sensor = (prx * xsf + pry * ysf) * ivn / (float)cam.sensor_w;
+    } else {
+        gcx = dl_ddist * hx; gcy = dl_ddist * hy; gcz = dl_ddist * hz + dl_dzeta;
+        g_sensor = -(dl_ddist * inv_dist) * (dvx * xsf + dvy * ysf) / (float)cam.sensor_w;
+        g_focal = 0.0f;
+    }
+    float *row = a.raw + (size_t)id * a.raw_stride;
+    red_add_v4(row, gcx, gcy, gcz, d_radius);
+    red_add_v4(row + 4, dl_do, g_focal, g_sensor, 1.0f);
+#pragma unroll
+    for (int i = 0; i < DP; i += 4) {
+        if (i < d) {  // DP is a multiple of 4 and up[] is zero beyond d
+            const float v0 = w * up[i], v1 = w * up[i + 1], v2 = w * up[i + 2], v3 = w * up[i + 3];
+            red_add_v4(row + 8 + i, v0, v1, v2, v3);
+        }
+    }
+}
+
+// KT > 0: K <= KT slots held in registers, every load of a phase issued before its first use
+// (the kernel is latency-bound on dependent gathers).  KT == 0: any K, slot by slot.
+#ifndef SS_BACKWARD_MINB
+#define SS_BACKWARD_MINB 2
+#endif
+template <int DP, int MODE, int KT>
+__global__ void __launch_bounds__(TILE_PX, (KT > 0) ? SS_BACKWARD_MINB : 1) k_backward(BackArgs a) {
     const Cam &cam = a.cam;
     const int tile = blockIdx.x;
     const int tid = threadIdx.x;
-    const int px = (tile % cam.ntx) * TILE + (tid & (TILE - 1));
-    const int py = (tile / cam.ntx) * TILE + (tid >> 4);
+    const int lane = tid & 31, warp = tid >> 5;
+    const int px = (tile % cam.ntx) * TILE + (((warp & 1) << 3) | (lane & 7));  // 8x4 block per warp
+    const int py = (tile / cam.ntx) * TILE + (((warp >> 1) << 2) | (lane >> 3));
     if (!(px < cam.W && py < cam.H)) return;
     const size_t P = (size_t)cam.W * cam.H;
     const size_t pix = (size_t)py * cam.W + px;
     const int K = a.K, d = a.d;
+    const int *__restrict__ ids = a.ids;
+    const float *__restrict__ zb = a.z;
+    const float *__restrict__ cb = a.clos;
 
-    if (a.ids[pix] < 0) {  // slots are filled front to back: an empty slot 0 means no hit
+    constexpr int KR = KT > 0 ? KT : 1;
+    int sid[KR]; float zk[KR], ck[KR];
+    if (KT > 0) {
+#pragma unroll
+        for (int k = 0; k < KR; ++k) {
+            const bool in = k < K;
+            sid[k] = in ? ids[k * P + pix] : -1;
+            zk[k] = in ? zb[k * P + pix] : 0.0f;
+            ck[k] = in ? cb[k * P + pix] : 0.0f;
+        }
         bool any = false;
-        for (int k = 1; k < K; ++k) any |= a.ids[k * P + pix] >= 0;
+#pragma unroll
+        for (int k = 0; k < KR; ++k) any |= sid[k] >= 0;
+        if (!any) return;
+    } else {
+        bool any = false;
+        for (int k = 0; k < K; ++k) any |= ids[k * P + pix] >= 0;
         if (!any) return;
     }
     const float ld = a.log_denom[pix];
@@ -59,19 +161,6 @@ __global__ void __launch_bounds__(TILE_PX) k_backward(BackArgs a) {
         up[i] = i < d ? a.upstream[pix * d + i] : 0.0f;
         fhat[i] = i < d ? w_bg * a.bg[i] : 0.0f;
     }
-    // f_hat from the stored slots only (grad.py:103-108)
-    for (int k = 0; k < K; ++k) {
-        const int id = a.ids[k * P + pix];
-        if (id < 0) continue;
-        const float o = a.rec[id].o;
-        const float E = expf(o * a.z[k * P + pix] * inv_g - ld);
-        const float w = o * a.clos[k * P + pix] * E;
-        const float *f = a.feat + (size_t)id * d;
-#pragma unroll
-        for (int i = 0; i < DP; ++i)
-            if (i < d) fhat[i] = fmaf(w, f[i], fhat[i]);
-    }
-
     // ray (camera.py:332-357)
     const double xs = ((px + 0.5) - cam.W / 2.0) * cam.pix;
     const double ys = ((py + 0.5) - cam.H / 2.0) * cam.pix;
@@ -81,67 +170,52 @@ __global__ void __launch_bounds__(TILE_PX) k_backward(BackArgs a) {
         ux = xs / vn; uy = ys / vn; uz = cam.focal / vn; inv_vnorm = 1.0 / vn;
     }
 
-    for (int k = 0; k < K; ++k) {
-        const int id = a.ids[k * P + pix];
-        if (id < 0) continue;
-        const Rec rc = a.rec[id];
-        const float o = rc.o;
-        const float zk = a.z[k * P + pix], ck = a.clos[k * P + pix];
-        const float ez = o * zk * inv_g;
-        const float E = expf(ez - ld);
-        const float w = o * ck * E;
-        const float *f = a.feat + (size_t)id * d;
-        float acoef = 0.0f;
+    if (KT > 0) {
+        // gather all records and features first, then f_hat (grad.py:103-108), then the gradients
+        Rec rc[KR];
+        float f[KR][DP];
 #pragma unroll
-        for (int i = 0; i < DP; ++i)
-            if (i < d) acoef = fmaf(up[i], f[i] - fhat[i], acoef);
-        const double dl_dz = (double)(acoef * w * o * inv_g);
-        const double dl_dc = (double)(acoef * o * E);
-        const float dl_do = acoef * ck * E * (1.0f + ez);
-
-        // geometry chain, float64 (grad.py:117-165)
-        const double r = (double)rc.r;
-        double t, dvx, dvy, dvz;
-        if (MODE == SS_MODE_PINHOLE) {
-            t = rc.cx * ux + rc.cy * uy + rc.cz * uz;
-            dvx = rc.cx - t * ux; dvy = rc.cy - t * uy; dvz = rc.cz - t * uz;
-        } else {
-            t = rc.cz;
-            dvx = rc.cx - xs; dvy = rc.cy - ys; dvz = 0.0;
-        }
-        const double dist = sqrt(fmax(dvx * dvx + dvy * dvy + dvz * dvz, 0.0));
-        const bool interior = (0.0f < zk) && (zk < 1.0f);
-        const double dl_dzeta = interior ? dl_dz * (-cam.inv_range) : 0.0;
-        const double dl_ddist = -dl_dc / fmax(r, 1e-300);
-        const double d_radius = dl_dc * dist / fmax(r * r, 1e-300);
-        const double inv_dist = dist > 1e-12 ? 1.0 / dist : 0.0;
-        const double hx = dvx * inv_dist, hy = dvy * inv_dist, hz = dvz * inv_dist;
-        double gcx, gcy, gcz, g_focal, g_sensor;
-        if (MODE == SS_MODE_PINHOLE) {
-            const double zu = dl_dzeta * uz;
-            gcx = dl_ddist * hx + zu * ux;
-            gcy = dl_ddist * hy + zu * uy;
-            gcz = dl_ddist * hz + zu * uz;
-            const double s1 = dl_ddist * (-t) * inv_dist + zu;
-            const double gux = s1 * rc.cx, guy = s1 * rc.cy, guz = s1 * rc.cz + dl_dzeta * t;
-            const double gdu = gux * ux + guy * uy + guz * uz;
-            const double prx = gux - gdu * ux, pry = guy - gdu * uy, prz = guz - gdu * uz;
-            g_focal = prz * inv_vnorm;
-            g_sensor = (prx * xs + pry * ys) * inv_vnorm / cam.sensor_w;
-        } else {
-            gcx = dl_ddist * hx; gcy = dl_ddist * hy; gcz = dl_ddist * hz + dl_dzeta;
-            g_sensor = -(dl_ddist * inv_dist) * (dvx * xs + dvy * ys) / cam.sensor_w;
-            g_focal = 0.0;
-        }
-        float *row = a.raw + (size_t)id * a.raw_stride;
-        red_add_v4(row, (float)gcx, (float)gcy, (float)gcz, (float)d_radius);
-        red_add_v4(row + 4, dl_do, (float)g_focal, (float)g_sensor, 1.0f);
+        for (int k = 0; k < KR; ++k) {
+            const int id = sid[k] >= 0 ? sid[k] : 0;
+            if (sid[k] >= 0) rc[k] = a.rec[id];
 #pragma unroll
-        for (int i = 0; i < DP; i += 4) {
-            if (i < d) {  // DP is a multiple of 4 and up[] is zero beyond d
-                const float v0 = w * up[i], v1 = w * up[i + 1], v2 = w * up[i + 2], v3 = w * up[i + 3];
-                red_add_v4(row + 8 + i, v0, v1, v2, v3);
+            for (int i = 0; i < DP; ++i) f[k][i] = (sid[k] >= 0 && i < d) ? a.feat[(size_t)id * d + i] : 0.0f;
+        }
+#pragma unroll
+        for (int k = 0; k < KR; ++k) {
+            if (sid[k] >= 0) {
+                const float E = expf(rc[k].o * zk[k] * inv_g - ld);
+                const float w = rc[k].o * ck[k] * E;
+#pragma unroll
+                for (int i = 0; i < DP; ++i) fhat[i] = fmaf(w, f[k][i], fhat[i]);
             }
+        }
+#pragma unroll
+        for (int k = 0; k < KR; ++k)
+            if (sid[k] >= 0)
+                slot_gradient<DP, MODE>(a, rc[k], sid[k], zk[k], ck[k], ld, inv_g, up, fhat, f[k], d, xs, ys, ux, uy,
+                                        uz, inv_vnorm);
+    } else {
+        for (int k = 0; k < K; ++k) {
+            const int id = ids[k * P + pix];
+            if (id < 0) continue;
+            const float o = a.rec[id].o;
+            const float E = expf(o * zb[k * P + pix] * inv_g - ld);
+            const float w = o * cb[k * P + pix] * E;
+            const float *f = a.feat + (size_t)id * d;
+#pragma unroll
+            for (int i = 0; i < DP; ++i)
+                if (i < d) fhat[i] = fmaf(w, f[i], fhat[i]);
+        }
+        for (int k = 0; k < K; ++k) {
+            const int id = ids[k * P + pix];
+            if (id < 0) continue;
+            const Rec rc = a.rec[id];
+            float f[DP];
+#pragma unroll
+            for (int i = 0; i < DP; ++i) f[i] = i < d ? a.feat[(size_t)id * d + i] : 0.0f;
+            slot_gradient<DP, MODE>(a, rc, id, zb[k * P + pix], cb[k * P + pix], ld, inv_g, up, fhat, f, d, xs, ys,
+                                    ux, uy, uz, inv_vnorm);
         }
     }
 }
@@ -165,8 +239,8 @@ __global__ void __launch_bounds__(256) k_finalize(FinArgs a) {
     double acc[14];
 #pragma unroll
     for (int j = 0; j < 14; ++j) acc[j] = 0.0;
-    const long long stride = (long long)gridDim.x * blockDim.x;
-    for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < a.M; i += stride) {
+    const long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i < a.M) {
         const float4 *row = (const float4 *)(a.raw + (size_t)i * a.raw_stride);
         const float4 r0 = row[0], r1 = row[1];
         const float cnt = r1.w;
@@ -195,12 +269,12 @@ __global__ void __launch_bounds__(256) k_finalize(FinArgs a) {
                 const double sx = cam_scale * gx, sy = cam_scale * gy, sz = cam_scale * gz;
                 const double rx = (double)a.pos[3 * i] - cam.t[0], ry = (double)a.pos[3 * i + 1] - cam.t[1],
                              rz = (double)a.pos[3 * i + 2] - cam.t[2];
-                acc[0] += sx; acc[1] += sy; acc[2] += sz;
-                acc[3] += sx * rx; acc[4] += sx * ry; acc[5] += sx * rz;
-                acc[6] += sy * rx; acc[7] += sy * ry; acc[8] += sy * rz;
-                acc[9] += sz * rx; acc[10] += sz * ry; acc[11] += sz * rz;
-                acc[12] += cam_scale * (double)r1.y;
-                acc[13] += cam_scale * (double)r1.z;
+                acc[0] = sx; acc[1] = sy; acc[2] = sz;
+                acc[3] = sx * rx; acc[4] = sx * ry; acc[5] = sx * rz;
+                acc[6] = sy * rx; acc[7] = sy * ry; acc[8] = sy * rz;
+                acc[9] = sz * rx; acc[10] = sz * ry; acc[11] = sz * rz;
+                acc[12] = cam_scale * (double)r1.y;
+                acc[13] = cam_scale * (double)r1.z;
             }
         } else if (!a.accumulate) {
             for (int k = 0; k < a.d; ++k) a.d_feat[(size_t)i * a.d + k] = 0.0f;
@@ -216,7 +290,8 @@ __global__ void __launch_bounds__(256) k_finalize(FinArgs a) {
         }
     }
     if (!a.cam_grads) return;
-    // block reduction of the 14 camera sums, then a fixed-order final pass by the last block
+    // block reduction of the 14 camera sums (float64), one double atomic per value and block into the
+    // global accumulators, then the last block to finish converts the sums into the camera block
     const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
 #pragma unroll
     for (int j = 0; j < 14; ++j) {
@@ -225,40 +300,42 @@ __global__ void __launch_bounds__(256) k_finalize(FinArgs a) {
         if (lane == 0) s_part[wid][j] = v;
     }
     __syncthreads();
+    double *sums = a.cam_part;  // 16 doubles, zeroed by launch_backward
     if (threadIdx.x < 14) {
         double v = 0.0;
         for (int w = 0; w < 8; ++w) v += s_part[w][threadIdx.x];
-        a.cam_part[(size_t)blockIdx.x * CAM_VALS + threadIdx.x] = v;
+        if (v != 0.0) atomicAdd(&sums[threadIdx.x], v);
     }
     __threadfence();
     __syncthreads();
-    unsigned int *counter = (unsigned int *)(a.cam_part + (size_t)CAM_BLOCKS_MAX * CAM_VALS);
+    unsigned int *counter = (unsigned int *)(a.cam_part + CAM_VALS);
     if (threadIdx.x == 0) s_last = (atomicAdd(counter, 1u) == gridDim.x - 1);
     __syncthreads();
     if (!s_last) return;
     __threadfence();
-    __shared__ double s_tot[14];
-    if (threadIdx.x < 14) {
-        double v = 0.0;
-        for (unsigned b = 0; b < gridDim.x; ++b) v += a.cam_part[(size_t)b * CAM_VALS + threadIdx.x];
-        s_tot[threadIdx.x] = v;
-    }
-    __syncthreads();
     if (threadIdx.x == 0) {
-        *counter = 0;  // ready for the next call
+        volatile double *vs = sums;
+        double t0 = vs[0], t1 = vs[1], t2 = vs[2];
         for (int j = 0; j < 3; ++j)  // d_translation = -(sum sc) @ R  (grad.py:289)
-            a.cam_grad[j] = -(s_tot[0] * R[0 + j] + s_tot[1] * R[3 + j] + s_tot[2] * R[6 + j]);
-        for (int j = 0; j < 9; ++j) a.cam_grad[3 + j] = s_tot[3 + j];
-        a.cam_grad[12] = s_tot[12];
-        a.cam_grad[13] = s_tot[13];
+            a.cam_grad[j] = -(t0 * R[0 + j] + t1 * R[3 + j] + t2 * R[6 + j]);
+        for (int j = 0; j < 9; ++j) a.cam_grad[3 + j] = vs[3 + j];
+        a.cam_grad[12] = vs[12];
+        a.cam_grad[13] = vs[13];
         a.cam_grad[14] = 0.0; a.cam_grad[15] = 0.0;
     }
 }
 
-template <int DP>
+template <int DP, int KT>
 void launch_bw_mode(const BackArgs &b, int n_tiles, int mode, cudaStream_t s) {
-    if (mode == SS_MODE_PINHOLE) k_backward<DP, SS_MODE_PINHOLE><<<n_tiles, TILE_PX, 0, s>>>(b);
-    else k_backward<DP, SS_MODE_ORTHOGRAPHIC><<<n_tiles, TILE_PX, 0, s>>>(b);
+    if (mode == SS_MODE_PINHOLE) k_backward<DP, SS_MODE_PINHOLE, KT><<<n_tiles, TILE_PX, 0, s>>>(b);
+    else k_backward<DP, SS_MODE_ORTHOGRAPHIC, KT><<<n_tiles, TILE_PX, 0, s>>>(b);
+}
+
+template <int DP>
+void launch_bw_k(const BackArgs &b, int n_tiles, int mode, cudaStream_t s) {
+    if (DP <= 4 && b.K <= 5) launch_bw_mode<DP, 5>(b, n_tiles, mode, s);
+    else if (DP <= 4 && b.K <= 8) launch_bw_mode<DP, 8>(b, n_tiles, mode, s);
+    else launch_bw_mode<DP, 0>(b, n_tiles, mode, s);
 }
 
 }  // namespace
@@ -277,7 +354,7 @@ cudaError_t launch_backward(const BwdLaunch &a, cudaStream_t s) {
         ProfScope ps(KID_MEMSET_BWD, s);
         e = cudaMemsetAsync(raw, 0, (size_t)M * L.raw_stride * sizeof(float), s);
         if (e != cudaSuccess) return e;
-        e = cudaMemsetAsync(a.ws + L.cam_part + (size_t)CAM_BLOCKS_MAX * CAM_VALS * 8, 0, 16, s);
+        e = cudaMemsetAsync(a.ws + L.cam_part, 0, (CAM_VALS + 2) * 8, s);  // camera sums + completion counter
         if (e != cudaSuccess) return e;
     }
     BackArgs b;
@@ -291,9 +368,9 @@ cudaError_t launch_backward(const BwdLaunch &a, cudaStream_t s) {
     const int d = b.d, mode = a.cam.mode;
     {
         ProfScope ps(KID_BACKWARD, s);
-        if (d <= 4) launch_bw_mode<4>(b, L.n_tiles, mode, s);
-        else if (d <= 16) launch_bw_mode<16>(b, L.n_tiles, mode, s);
-        else launch_bw_mode<32>(b, L.n_tiles, mode, s);
+        if (d <= 4) launch_bw_k<4>(b, L.n_tiles, mode, s);
+        else if (d <= 16) launch_bw_k<16>(b, L.n_tiles, mode, s);
+        else launch_bw_k<32>(b, L.n_tiles, mode, s);
     }
 
     FinArgs f;
@@ -308,8 +385,7 @@ cudaError_t launch_backward(const BwdLaunch &a, cudaStream_t s) {
     f.gate = (a.blend.flags & SS_OPT_GATE) ? 1 : 0;
     f.cam_grads = cam_grads ? 1 : 0;
     f.accumulate = (a.blend.flags & SS_OPT_ACCUMULATE) ? 1 : 0;
-    long long blocks = (M + 255) / 256;
-    int grid = (int)(blocks < CAM_BLOCKS_MAX ? blocks : CAM_BLOCKS_MAX);
+    int grid = (int)((M + 255) / 256);
     {
         ProfScope ps(KID_FINALIZE, s);
         k_finalize<<<grid, 256, 0, s>>>(f);

@@ -32,13 +32,15 @@ struct Cam {
 // Workspace layout (byte offsets, 256-byte aligned).
 struct Layout {
     size_t status;       // 16 x int64 (SsStatus)
-    size_t tile_count;   // n_tiles + 1 int32 (zeroed with status at forward start)
+    size_t tile_count;   // n_tiles + 1 int32 (zeroed with status at forward start): spheres touching <= 4 tiles
+    size_t tile_count_big;  // n_tiles + 1 int32 (zeroed too): spheres touching > 4 tiles
     size_t tile_start;   // n_tiles + 1 int32
     size_t tile_cursor;  // n_tiles int32
     size_t big_tiles;    // n_tiles + 1 int32: [0] = count, then tile ids with > SORT_SMALL pairs
     size_t rec;          // M Rec
     size_t key;          // M uint64 (order-preserving bits of earliest)
     size_t trect;        // M ushort4 tile rects (tx0, tx1, ty0, ty1); tx0 > tx1 = off sensor
+    size_t slot4;        // M int4: slot inside each touched tile's segment (spheres touching <= 4 tiles)
     size_t proj_r;       // M double
     size_t pair_key;     // max_pairs uint64
     size_t pair_id;      // max_pairs int32
@@ -71,12 +73,14 @@ inline Layout make_layout(const SsDims &dm) {
     auto take = [&](size_t bytes) { size_t o = off; off = align256(off + bytes); return o; };
     L.status = take(16 * sizeof(int64_t));
     L.tile_count = take((size_t)(L.n_tiles + 1) * 4);
+    L.tile_count_big = take((size_t)(L.n_tiles + 1) * 4);
     L.tile_start = take((size_t)(L.n_tiles + 1) * 4);
     L.tile_cursor = take((size_t)L.n_tiles * 4);
     L.big_tiles = take((size_t)(L.n_tiles + 1) * 4);
     L.rec = take(M * sizeof(Rec));
     L.key = take(M * 8);
     L.trect = take(M * 8);
+    L.slot4 = take(M * 16);
     L.proj_r = take(M * 8);
     L.pair_key = take(P * 8);
     L.pair_id = take(P * 4);

@@ -5,7 +5,10 @@
 //               validation (scene.py:91-114) -- float64 per sphere, M-parallel, plus the
 //               per-tile candidate COUNT (one atomic per touched tile).
 //   k_scan      exclusive prefix sum of the tile counts -> tile_start (raster.py:290-292).
-//   k_emit      writes each (tile, sphere) pair into its tile's segment.
+//   k_emit      writes each (tile, sphere) pair into its tile's segment.  The slot inside the
+//               segment was already claimed by k_project's counting atomic (spheres touching
+//               <= 4 tiles, i.e. nearly all), so k_emit is a pure streaming pass; spheres that
+//               touch more tiles claim their slots here, behind the pre-claimed ones.
 //   k_tile_sort per-tile sort of the segment by (earliest float64, sphere index): exactly the
 //               order the reference gets from "stable argsort by earliest" (raster.py:243)
 //               followed by "stable argsort by tile id" (raster.py:289).  One CTA per tile,
@@ -72,7 +75,7 @@ struct ProjectArgs {
     const float *pos, *rad, *opa, *feat, *bg;
     Cam cam;
     Rec *rec; unsigned long long *key; ushort4 *trect; double *proj_r;
-    int *tile_count; long long *status;
+    int *tile_count; int *tile_count_big; int4 *slot4; long long *status;
     int32_t *rect; uint8_t *on_sensor; double *earliest; double *proj_r_out;
     int records_only; int validate;
 };
@@ -146,8 +149,17 @@ __global__ void __launch_bounds__(256) k_project(ProjectArgs a) {
             if (on) {
                 tr.x = (unsigned short)(x0 / TILE); tr.y = (unsigned short)(x1 / TILE);
                 tr.z = (unsigned short)(y0 / TILE); tr.w = (unsigned short)(y1 / TILE);
-                for (int ty = tr.z; ty <= tr.w; ++ty)
-                    for (int tx = tr.x; tx <= tr.y; ++tx) atomicAdd(&a.tile_count[ty * cam.ntx + tx], 1);
+                const int wx = tr.y - tr.x + 1, nt = wx * (tr.w - tr.z + 1);
+                if (nt <= 4) {  // claim the slots now; k_emit needs no atomics for this sphere
+                    int sl[4] = {0, 0, 0, 0};
+#pragma unroll
+                    for (int j = 0; j < 4; ++j)
+                        if (j < nt) sl[j] = atomicAdd(&a.tile_count[(tr.z + j / wx) * cam.ntx + tr.x + j % wx], 1);
+                    a.slot4[i] = make_int4(sl[0], sl[1], sl[2], sl[3]);
+                } else {
+                    for (int ty = tr.z; ty <= tr.w; ++ty)
+                        for (int tx = tr.x; tx <= tr.y; ++tx) atomicAdd(&a.tile_count_big[ty * cam.ntx + tx], 1);
+                }
             } else {
                 tr.x = 1; tr.y = 0; tr.z = 1; tr.w = 0;
             }
@@ -163,7 +175,8 @@ __global__ void __launch_bounds__(256) k_project(ProjectArgs a) {
 
 // Single-CTA exclusive scan over the tile counts; also resets the emit cursors, lists the
 // tiles whose segment is too long for the small sort kernel, and publishes T / overflow.
-__global__ void __launch_bounds__(1024) k_scan(const int *__restrict__ tile_count, int *tile_start,
+__global__ void __launch_bounds__(1024) k_scan(const int *__restrict__ tile_count,
+                                               const int *__restrict__ tile_count_big, int *tile_start,
                                                int *tile_cursor, int *big_tiles, int n_tiles,
                                                long long max_pairs, long long M, long long *status) {
     __shared__ long long warp_sums[32];
@@ -174,7 +187,8 @@ __global__ void __launch_bounds__(1024) k_scan(const int *__restrict__ tile_coun
     __syncthreads();
     for (int base = 0; base < n_tiles; base += 1024) {
         int i = base + tid;
-        int c = i < n_tiles ? tile_count[i] : 0;
+        const int c_small = i < n_tiles ? tile_count[i] : 0;
+        int c = c_small + (i < n_tiles ? tile_count_big[i] : 0);
         long long v = c;
         for (int o = 1; o < 32; o <<= 1) {
             long long n = __shfl_up_sync(0xffffffffu, v, o);
@@ -195,7 +209,7 @@ __global__ void __launch_bounds__(1024) k_scan(const int *__restrict__ tile_coun
         long long excl = carry + (wid ? warp_sums[wid - 1] : 0) + v - c;
         if (i < n_tiles) {
             tile_start[i] = (int)(excl > 0x7fffffffLL ? 0x7fffffffLL : excl);
-            tile_cursor[i] = 0;
+            tile_cursor[i] = c_small;  // late claims (k_emit) go behind the pre-claimed slots
             if (c > SORT_SMALL) big_tiles[1 + atomicAdd(&n_big, 1)] = i;
         }
         __syncthreads();
@@ -214,6 +228,7 @@ __global__ void __launch_bounds__(1024) k_scan(const int *__restrict__ tile_coun
 }
 
 __global__ void __launch_bounds__(256) k_emit(long long M, const ushort4 *__restrict__ trect,
+                                              const int4 *__restrict__ slot4,
                                               const unsigned long long *__restrict__ key,
                                               const int *__restrict__ tile_start, int *tile_cursor,
                                               unsigned long long *pair_key, int *pair_id, int ntx,
@@ -224,6 +239,19 @@ __global__ void __launch_bounds__(256) k_emit(long long M, const ushort4 *__rest
     ushort4 tr = trect[i];
     if (tr.x > tr.y) return;
     unsigned long long k = key[i];
+    const int wx = tr.y - tr.x + 1, nt = wx * (tr.w - tr.z + 1);
+    if (nt <= 4) {
+        const int4 s4 = slot4[i];
+        const int sl[4] = {s4.x, s4.y, s4.z, s4.w};
+#pragma unroll
+        for (int j = 0; j < 4; ++j)
+            if (j < nt) {
+                const int pos = tile_start[(tr.z + j / wx) * ntx + tr.x + j % wx] + sl[j];
+                pair_key[pos] = k;
+                pair_id[pos] = (int)i;
+            }
+        return;
+    }
     for (int ty = tr.z; ty <= tr.w; ++ty)
         for (int tx = tr.x; tx <= tr.y; ++tx) {
             int t = ty * ntx + tx;
@@ -323,7 +351,7 @@ cudaError_t launch_project(const FwdLaunch &a, bool records_only, cudaStream_t s
     char *ws = a.ws;
     const Layout &L = a.L;
     if (!records_only) {
-        // status + tile_count are contiguous: one memset
+        // status + tile_count + tile_count_big are contiguous: one memset
         ProfScope ps(KID_MEMSET_FWD, s);
         cudaError_t e = cudaMemsetAsync(ws + L.status, 0, L.tile_start - L.status, s);
         if (e != cudaSuccess) return e;
@@ -335,7 +363,8 @@ cudaError_t launch_project(const FwdLaunch &a, bool records_only, cudaStream_t s
         p.cam = a.cam;
         p.rec = (Rec *)(ws + L.rec); p.key = (unsigned long long *)(ws + L.key);
         p.trect = (ushort4 *)(ws + L.trect); p.proj_r = (double *)(ws + L.proj_r);
-        p.tile_count = (int *)(ws + L.tile_count); p.status = (long long *)(ws + L.status);
+        p.tile_count = (int *)(ws + L.tile_count); p.tile_count_big = (int *)(ws + L.tile_count_big);
+        p.slot4 = (int4 *)(ws + L.slot4); p.status = (long long *)(ws + L.status);
         p.rect = a.rect; p.on_sensor = a.on_sensor; p.earliest = a.earliest; p.proj_r_out = a.proj_r_out;
         p.records_only = records_only ? 1 : 0;
         p.validate = (!records_only && !(a.blend.flags & SS_OPT_SKIP_VALIDATE)) ? 1 : 0;
@@ -359,15 +388,15 @@ cudaError_t launch_binning(const FwdLaunch &a, cudaStream_t s) {
     int *pair_id = (int *)(ws + L.pair_id);
     {
         ProfScope ps(KID_SCAN, s);
-        k_scan<<<1, 1024, 0, s>>>((const int *)(ws + L.tile_count), tile_start, tile_cursor, big_tiles,
-                                  L.n_tiles, a.dims.max_pairs, M, status);
+        k_scan<<<1, 1024, 0, s>>>((const int *)(ws + L.tile_count), (const int *)(ws + L.tile_count_big),
+                                  tile_start, tile_cursor, big_tiles, L.n_tiles, a.dims.max_pairs, M, status);
     }
     count_launch();
     if (M > 0) {
         unsigned grid = (unsigned)((M + 255) / 256);
         {
             ProfScope ps(KID_EMIT, s);
-            k_emit<<<grid, 256, 0, s>>>(M, (const ushort4 *)(ws + L.trect),
+            k_emit<<<grid, 256, 0, s>>>(M, (const ushort4 *)(ws + L.trect), (const int4 *)(ws + L.slot4),
                                         (const unsigned long long *)(ws + L.key), tile_start, tile_cursor,
                                         pair_key, pair_id, L.ntx, status);
         }

@@ -74,7 +74,7 @@ struct ProjectArgs {
     long long M; int d;
     const float *pos, *rad, *opa, *feat, *bg;
     Cam cam;
-    Rec *rec; unsigned long long *key; ushort4 *trect; double *proj_r;
+    Rec *rec; unsigned long long *key; ushort4 *trect; double *proj_r; float4 *flt;
     int *tile_count; int *tile_count_big; int4 *slot4; long long *status;
     int32_t *rect; uint8_t *on_sensor; double *earliest; double *proj_r_out;
     int records_only; int validate;
@@ -133,6 +133,31 @@ __global__ void __launch_bounds__(256) k_project(ProjectArgs a) {
         }
         a.proj_r[i] = pr;
         if (a.proj_r_out) a.proj_r_out[i] = pr;
+        if (!a.records_only) {
+            // Screen-space filter record for k_raster: a pixel can only hit the sphere if it lies in
+            // the circle around the projected centre with radius f (tan(theta + alpha) - tan(theta))
+            // (theta: centre off the optical axis, alpha = asin(r/|c|)), which bounds the projected
+            // outline.  Padded for the float32 evaluation; infinite (always passes) when the sphere
+            // reaches the camera plane or contains the camera.
+            double pcx = 0.0, pcy = 0.0, rho = INFINITY;
+            if (cam.mode == SS_MODE_PINHOLE) {
+                const double n2 = cx * cx + cy * cy + cz * cz, rr = r * r;
+                if (cz > r && n2 > rr) {
+                    const double tan_t = sqrt(cx * cx + cy * cy) / cz;
+                    const double tan_a = r / sqrt(n2 - rr);
+                    const double den = 1.0 - tan_t * tan_a;
+                    if (den > 1e-6) {
+                        rho = cam.focal * ((tan_t + tan_a) / den - tan_t);
+                        pcx = cam.focal * cx / cz;
+                        pcy = cam.focal * cy / cz;
+                    }
+                }
+            } else {
+                pcx = cx; pcy = cy; rho = r;
+            }
+            const float rho_pad = (float)(rho * (1.0 + 1e-5) + 4e-7 * (fabs(pcx) + fabs(pcy) + cam.sensor_w));
+            a.flt[i] = make_float4((float)pcx, (float)pcy, rho_pad * rho_pad * 1.000001f, 0.0f);
+        }
         if (!a.records_only) {
             int x0, x1, y0, y1; bool out_x, out_y;
             discretize_extent(w / 2.0 + lo_x * cam.ppu, w / 2.0 + hi_x * cam.ppu, u_c, w, x0, x1, out_x);
@@ -363,6 +388,7 @@ cudaError_t launch_project(const FwdLaunch &a, bool records_only, cudaStream_t s
         p.cam = a.cam;
         p.rec = (Rec *)(ws + L.rec); p.key = (unsigned long long *)(ws + L.key);
         p.trect = (ushort4 *)(ws + L.trect); p.proj_r = (double *)(ws + L.proj_r);
+        p.flt = (float4 *)(ws + L.flt);
         p.tile_count = (int *)(ws + L.tile_count); p.tile_count_big = (int *)(ws + L.tile_count_big);
         p.slot4 = (int4 *)(ws + L.slot4); p.status = (long long *)(ws + L.status);
         p.rect = a.rect; p.on_sensor = a.on_sensor; p.earliest = a.earliest; p.proj_r_out = a.proj_r_out;

@@ -26,6 +26,7 @@ struct RasterArgs {
     const int *tile_start;
     const int *pair_id;
     const Rec *rec;
+    const float4 *flt;
     const float *feat;
     const float *bg;
     int d, K, chunk;
@@ -109,6 +110,10 @@ __global__ void __launch_bounds__(TILE_PX, (KT <= 8 && DP <= 4) ? SS_RASTER_MINB
     double *s_cx = (double *)(s_misc + CAP);       // float64 centre and |c|^2 for the exact decision
     double *s_cy = s_cx + CAP, *s_cz = s_cy + CAP, *s_n2 = s_cz + CAP;
     float *s_f = (float *)(s_n2 + CAP);            // features, DP per candidate
+    unsigned char *s_wmask = (unsigned char *)(s_f + CAP * DP);  // per candidate: which warps' pixel blocks it can touch
+    unsigned char *s_list = s_wmask + CAP;         // per warp: compacted indices of its relevant candidates
+    constexpr int LSTRIDE = CAP + 4;
+    __shared__ float4 s_rect[8];                   // per warp: sensor-space rectangle of its pixel centres
     __shared__ double s_red[8];
     __shared__ unsigned long long s_stat[3];
 
@@ -138,6 +143,15 @@ __global__ void __launch_bounds__(TILE_PX, (KT <= 8 && DP <= 4) ? SS_RASTER_MINB
     float fx = valid ? (float)xs : kFar;
     float fy = (float)ys;
     fx = pin_reg(fx); fy = pin_reg(fy);
+    {   // sensor-space rectangle spanned by this warp's in-image pixel centres (empty: +inf/-inf)
+        float x0 = valid ? (float)xs : INFINITY, x1 = valid ? (float)xs : -INFINITY;
+        float y0 = valid ? (float)ys : INFINITY, y1 = valid ? (float)ys : -INFINITY;
+        for (int o = 16; o > 0; o >>= 1) {
+            x0 = fminf(x0, __shfl_xor_sync(0xffffffffu, x0, o)); x1 = fmaxf(x1, __shfl_xor_sync(0xffffffffu, x1, o));
+            y0 = fminf(y0, __shfl_xor_sync(0xffffffffu, y0, o)); y1 = fmaxf(y1, __shfl_xor_sync(0xffffffffu, y1, o));
+        }
+        if (lane == 0) s_rect[warp] = make_float4(x0, x1, y0, y1);
+    }
 
     const bool overflow = (a.status[ST_FLAGS] & SS_FLAG_PAIR_OVERFLOW) != 0;  // lists not built
     const int s0 = a.tile_start[tile];
@@ -220,7 +234,6 @@ __global__ void __launch_bounds__(TILE_PX, (KT <= 8 && DP <= 4) ? SS_RASTER_MINB
 
     for (int start = 0; start < n_cand; start += a.chunk) {
         const int cn = min(a.chunk, n_cand - start);
-        const int cn4 = (cn + 3) & ~3;
         __syncthreads();  // previous batch fully consumed
         if (tid < cn) {
             const int sid = a.pair_id[s0 + start + tid];
@@ -228,32 +241,23 @@ __global__ void __launch_bounds__(TILE_PX, (KT <= 8 && DP <= 4) ? SS_RASTER_MINB
             const double n2 = rc.cx * rc.cx + rc.cy * rc.cy + rc.cz * rc.cz;
             s_cx[tid] = rc.cx; s_cy[tid] = rc.cy; s_cz[tid] = rc.cz; s_n2[tid] = n2;
             s_misc[tid] = make_float4(rc.r, rc.o, rc.o * inv_g2, __int_as_float(sid));
-            // screen-space filter record: projected centre and bounding-circle radius (float64
-            // here, once per candidate; float32 + rounding pad in the test loop)
-            double pcx, pcy, rho;
-            if (MODE == SS_MODE_PINHOLE) {
-                const double rr = (double)rc.r * (double)rc.r;
-                rho = INFINITY; pcx = 0.0; pcy = 0.0;  // default: always passes (camera near/inside the sphere)
-                if (rc.cz > (double)rc.r && n2 > rr) {
-                    const double tan_t = sqrt(rc.cx * rc.cx + rc.cy * rc.cy) / rc.cz;
-                    const double tan_a = (double)rc.r / sqrt(n2 - rr);
-                    const double den = 1.0 - tan_t * tan_a;
-                    if (den > 1e-6) {
-                        rho = cam.focal * ((tan_t + tan_a) / den - tan_t);
-                        pcx = cam.focal * rc.cx / rc.cz;
-                        pcy = cam.focal * rc.cy / rc.cz;
-                    }
-                }
-            } else {
-                pcx = rc.cx; pcy = rc.cy; rho = (double)rc.r;
+            const float4 fc = a.flt[sid];  // screen-space filter record (k_project)
+            s_cf[tid] = fc;
+            // which warps can this candidate touch?  Same arithmetic as the per-pixel test, applied to the
+            // point of the warp's rectangle nearest to the projected centre (rounding is monotone, so a
+            // pixel can pass the test only if its warp's rectangle does)
+            unsigned wm = 0;
+#pragma unroll
+            for (int w = 0; w < 8; ++w) {
+                const float4 rc4 = s_rect[w];
+                const float dx = fminf(fmaxf(fc.x, rc4.x), rc4.y) - fc.x;
+                const float dy = fminf(fmaxf(fc.y, rc4.z), rc4.w) - fc.y;
+                wm |= (fmaf(dx, dx, dy * dy) < fc.z ? 1u : 0u) << w;
             }
-            const float rho_pad = (float)(rho * (1.0 + 1e-5) + 4e-7 * (fabs(pcx) + fabs(pcy) + cam.sensor_w));
-            s_cf[tid] = make_float4((float)pcx, (float)pcy, rho_pad * rho_pad * 1.000001f, 0.0f);
+            s_wmask[tid] = (unsigned char)wm;
             const float *f = a.feat + (size_t)sid * a.d;
 #pragma unroll
             for (int i = 0; i < DP; ++i) s_f[tid * DP + i] = i < a.d ? f[i] : 0.0f;
-        } else if (tid < cn4) {
-            s_cf[tid] = make_float4(0.f, 0.f, -1.0f, 0.f);  // padding: never passes the filter
         }
         __syncthreads();
         if (a.tau_on) {  // vote, raster.py:364-368
@@ -270,33 +274,47 @@ __global__ void __launch_bounds__(TILE_PX, (KT <= 8 && DP <= 4) ? SS_RASTER_MINB
         scanned += cn;
         if (__all_sync(0xffffffffu, done)) continue;  // warp-uniform
 
-        // float32 filter over the batch, 4 candidates per step.  The sign bits of (d^2 - rho^2) are
+        // compact the indices of the candidates that can touch this warp's 8x4 block (~1 in 4)
+        unsigned char *lst = s_list + warp * LSTRIDE;
+        int cnt = 0;
+        for (int base = 0; base < cn; base += 32) {
+            const int j = base + lane;
+            const bool rel = j < cn && ((s_wmask[j] >> warp) & 1u);
+            const unsigned bal = __ballot_sync(0xffffffffu, rel);
+            if (rel) lst[cnt + __popc(bal & ((1u << lane) - 1u))] = (unsigned char)j;
+            cnt += __popc(bal);
+        }
+        if (lane < 4) lst[cnt + lane] = 0;  // padding of the last group of 4: a readable slot, masked out below
+        __syncwarp();
+
+        // float32 filter over the relevant candidates, 4 per step.  The sign bits of (d^2 - rho^2) are
         // funnel-shifted into a 4-bit mask; a non-empty mask is pushed as one 10-bit entry
-        // [group:6 | mask:4] into a per-lane FIFO (6 entries in 64 bits).  The warp drains the
-        // FIFOs together, so the float64 path below runs with most lanes active.
+        // [group:6 | mask:4] into a per-lane FIFO (6 entries in 64 bits).  The warp drains the FIFOs
+        // together, so the float64 path runs with most lanes active.
         unsigned long long q = 0;
         int qn = 0;
         unsigned cur = 0;  // entry being consumed
         auto drain_round = [&]() {
             if ((cur & 15u) == 0u && qn > 0) { --qn; cur = (unsigned)(q >> (10 * qn)) & 0x3ffu; }
             if (cur & 15u) {
-                const int bit = 31 - __clz((int)(cur & 15u));  // candidate u sits at bit 3 - u
-                const int j = (int)((cur >> 4) << 2) + (3 - bit);
+                const int bit = 31 - __clz((int)(cur & 15u));  // candidate u of the group sits at bit 3 - u
+                const int j = lst[(int)((cur >> 4) << 2) + (3 - bit)];
                 cur &= ~(1u << bit);
                 process(j);
             }
         };
-        for (int j0 = 0; j0 < cn4; j0 += 4) {
+        for (int k = 0; k < cnt; k += 4) {
+            const unsigned idx4 = *reinterpret_cast<const unsigned *>(lst + k);
             unsigned acc = 0;
 #pragma unroll
             for (int u = 0; u < 4; ++u) {
-                const float4 c = s_cf[j0 + u];
+                const float4 c = s_cf[(idx4 >> (8 * u)) & 0xffu];
                 const float dx = fx - c.x, dy = fy - c.y;
                 const float sgn = fmaf(dx, dx, dy * dy) - c.z;  // negative = inside the bounding circle
                 acc = __funnelshift_l(__float_as_uint(sgn), acc, 1);
             }
-            acc &= 15u;
-            if (acc) { q = (q << 10) | (unsigned long long)(((unsigned)j0 << 2) | acc); ++qn; }
+            acc &= (cnt - k >= 4) ? 15u : ((0xF0u >> (cnt - k)) & 15u);
+            if (acc) { q = (q << 10) | (unsigned long long)(((unsigned)k << 2) | acc); ++qn; }
             if (__any_sync(0xffffffffu, qn >= 6)) {
                 while (true) {
                     const unsigned act = __ballot_sync(0xffffffffu, qn > 0 || (cur & 15u));
@@ -364,7 +382,9 @@ __global__ void __launch_bounds__(TILE_PX, (KT <= 8 && DP <= 4) ? SS_RASTER_MINB
 }
 
 template <int DP>
-constexpr size_t raster_smem_bytes() { return (size_t)SS_MAX_CHUNK * (16 + 16 + 32 + 4 * DP); }
+constexpr size_t raster_smem_bytes() {
+    return (size_t)SS_MAX_CHUNK * (16 + 16 + 32 + 4 * DP) + SS_MAX_CHUNK + 8 * (SS_MAX_CHUNK + 4);
+}
 
 template <int DP, int KT, int MODE>
 void launch_one(const RasterArgs &r, int n_tiles, cudaStream_t s) {
@@ -401,6 +421,7 @@ cudaError_t launch_raster(const FwdLaunch &a, cudaStream_t s) {
     r.tile_start = (const int *)(a.ws + L.tile_start);
     r.pair_id = (const int *)(a.ws + L.pair_id);
     r.rec = (const Rec *)(a.ws + L.rec);
+    r.flt = (const float4 *)(a.ws + L.flt);
     r.feat = a.feat; r.bg = a.bg;
     r.d = a.dims.feature_dim; r.K = a.dims.top_k; r.chunk = a.blend.chunk;
     r.gamma = a.gamma; r.eps_over_g = a.blend.eps / a.gamma;

@@ -33,6 +33,17 @@ __device__ __forceinline__ double clampd(double x, double lo, double hi) {
 __device__ void axis_extent_pinhole(double ca, double cz, double r, double focal, double &lo,
                                     double &hi, bool &empty) {
     double n2 = ca * ca + cz * cz;
+    if (cz > r * 1.000001 && n2 > r * r) {
+        // Disc strictly in front of the camera plane: |phi| + beta < pi/2, so the wedge neither crosses
+        // the horizon nor is empty or full, and tan(phi -+ beta) has the closed form below (same value
+        // as the reference's asin/atan2/tan chain to a few ulp, at a third of the FP64 instructions).
+        const double tb = r / sqrt(n2 - r * r);  // tan(beta), beta = asin(r / n)
+        const double tp = ca / cz;               // tan(phi), phi = atan2(ca, cz)
+        lo = focal * ((tp - tb) / (1.0 + tp * tb));
+        hi = focal * ((tp + tb) / (1.0 - tp * tb));
+        empty = false;
+        return;
+    }
     double n = sqrt(n2);
     bool full = n2 <= r * r;
     double beta = asin(clampd(r / fmax(n, 1e-300), 0.0, 1.0));
@@ -328,19 +339,115 @@ __device__ void bitonic_sort_cta(KeyPtr keys, IdPtr ids, int n) {
     }
 }
 
+// ---- small segments: hybrid register / shared-memory bitonic sort -------------------------------
+// The first version ran all log2(n)(log2(n)+1)/2 stages through shared memory and was bound by
+// shared-memory bandwidth and barriers (ncu: l1tex 87 %, barrier stall 4.3).  Here every stage whose
+// partner distance is < 64 runs in registers: a warp holds a 64-element block (two per lane) and
+// exchanges with shuffles; only the flip and the j >= 64 disperse stages of the k >= 128 merges touch
+// shared memory (6 of 45 stages at n = 512).  Segments are padded to a power of two with +inf keys.
+struct El { unsigned long long k; int id; };
+
+__device__ __forceinline__ bool el_less(const El &a, const El &b) { return a.k < b.k || (a.k == b.k && a.id < b.id); }
+__device__ __forceinline__ El el_shfl_xor(const El &e, int m) {
+    El r;
+    r.k = __shfl_xor_sync(0xffffffffu, e.k, m);
+    r.id = __shfl_xor_sync(0xffffffffu, e.id, m);
+    return r;
+}
+__device__ __forceinline__ void el_keep(El &e, const El &p, bool keep_min) {
+    const bool p_less = el_less(p, e);
+    if (p_less == keep_min) e = p;  // keep_min: take the partner if it is smaller; else if it is not smaller
+}
+// partner lane = lane ^ m for both halves
+__device__ __forceinline__ void warp_stage(El &e0, El &e1, int m, bool keep_min) {
+    const El p0 = el_shfl_xor(e0, m), p1 = el_shfl_xor(e1, m);
+    el_keep(e0, p0, keep_min);
+    el_keep(e1, p1, keep_min);
+}
+// disperse stages j = 32, 16, ..., 1 on a 64-element block held as (e0 = block[lane], e1 = block[lane + 32])
+__device__ __forceinline__ void warp_disperse64(El &e0, El &e1, int lane) {
+    if (el_less(e1, e0)) { const El t = e0; e0 = e1; e1 = t; }  // j = 32
+#pragma unroll
+    for (int j = 16; j >= 1; j >>= 1) warp_stage(e0, e1, j, (lane & j) == 0);
+}
+// full sort of the 64-element block: merges k = 2 .. 64
+__device__ __forceinline__ void warp_sort64(El &e0, El &e1, int lane) {
+#pragma unroll
+    for (int k = 2; k <= 32; k <<= 1) {
+        warp_stage(e0, e1, k - 1, (lane & (k >> 1)) == 0);  // flip: i <-> i ^ (k - 1)
+#pragma unroll
+        for (int j = k >> 2; j >= 1; j >>= 1) warp_stage(e0, e1, j, (lane & j) == 0);
+    }
+    {   // flip of the k = 64 merge: index i <-> 63 - i, i.e. my e0 with e1 of lane ^ 31 and vice versa
+        const El p1 = el_shfl_xor(e1, 31), p0 = el_shfl_xor(e0, 31);
+        el_keep(e0, p1, true);
+        el_keep(e1, p0, false);
+    }
+#pragma unroll
+    for (int j = 16; j >= 1; j >>= 1) warp_stage(e0, e1, j, (lane & j) == 0);
+}
+
 __global__ void __launch_bounds__(256) k_tile_sort_small(const int *__restrict__ tile_start,
                                                          const unsigned long long *__restrict__ pair_key,
                                                          int *pair_id, const long long *__restrict__ status) {
     __shared__ unsigned long long keys[SORT_SMALL];
     __shared__ int ids[SORT_SMALL];
     if (status[ST_FLAGS] & SS_FLAG_PAIR_OVERFLOW) return;
-    int t = blockIdx.x;
-    int s0 = tile_start[t], n = tile_start[t + 1] - s0;
+    const int t = blockIdx.x;
+    const int s0 = tile_start[t], n = tile_start[t + 1] - s0;
     if (n < 2 || n > SORT_SMALL) return;
-    for (int i = threadIdx.x; i < n; i += blockDim.x) { keys[i] = pair_key[s0 + i]; ids[i] = pair_id[s0 + i]; }
+    int np2 = 64;
+    while (np2 < n) np2 <<= 1;
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const int n_blocks = np2 >> 6;
+    // load straight into registers, sort each 64-block (merges k = 2..64), park in shared memory
+    for (int b = warp; b < n_blocks; b += 8) {
+        const int i0 = (b << 6) + lane, i1 = i0 + 32;
+        El e0, e1;
+        e0.k = i0 < n ? pair_key[s0 + i0] : ~0ull; e0.id = i0 < n ? pair_id[s0 + i0] : 0x7fffffff;
+        e1.k = i1 < n ? pair_key[s0 + i1] : ~0ull; e1.id = i1 < n ? pair_id[s0 + i1] : 0x7fffffff;
+        warp_sort64(e0, e1, lane);
+        if (np2 == 64) {  // done: single block
+            if (i0 < n) pair_id[s0 + i0] = e0.id;
+            if (i1 < n) pair_id[s0 + i1] = e1.id;
+        } else {
+            keys[i0] = e0.k; ids[i0] = e0.id; keys[i1] = e1.k; ids[i1] = e1.id;
+        }
+    }
+    if (np2 == 64) return;
     __syncthreads();
-    bitonic_sort_cta(keys, ids, n);
-    for (int i = threadIdx.x; i < n; i += blockDim.x) pair_id[s0 + i] = ids[i];
+    const int half = np2 >> 1;
+    for (int k = 128; k <= np2; k <<= 1) {
+        const int hk = k >> 1;
+        for (int c = threadIdx.x; c < half; c += blockDim.x) {  // flip, shared memory
+            const int p = c & (hk - 1);
+            const int base = (c - p) << 1;
+            cas(keys, ids, base + p, base + k - 1 - p);
+        }
+        __syncthreads();
+        for (int j = hk >> 1; j >= 64; j >>= 1) {  // long-distance disperse stages, shared memory
+            for (int c = threadIdx.x; c < half; c += blockDim.x) {
+                const int p = c & (j - 1);
+                const int l = ((c - p) << 1) + p;
+                cas(keys, ids, l, l + j);
+            }
+            __syncthreads();
+        }
+        const bool last = (k == np2);
+        for (int b = warp; b < n_blocks; b += 8) {  // j = 32 .. 1 in registers
+            const int i0 = (b << 6) + lane, i1 = i0 + 32;
+            El e0, e1;
+            e0.k = keys[i0]; e0.id = ids[i0]; e1.k = keys[i1]; e1.id = ids[i1];
+            warp_disperse64(e0, e1, lane);
+            if (last) {
+                if (i0 < n) pair_id[s0 + i0] = e0.id;
+                if (i1 < n) pair_id[s0 + i1] = e1.id;
+            } else {
+                keys[i0] = e0.k; ids[i0] = e0.id; keys[i1] = e1.k; ids[i1] = e1.id;
+            }
+        }
+        if (!last) __syncthreads();
+    }
 }
 
 // Persistent over the list of long segments: <= SORT_BIG in dynamic smem, longer in place.

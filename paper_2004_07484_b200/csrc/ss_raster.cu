@@ -15,6 +15,8 @@
 // Eq. 1) runs in float32.
 #include <math.h>
 
+#include <type_traits>
+
 #include "ss_common.cuh"
 
 namespace ss {
@@ -51,6 +53,10 @@ struct TopK {
             for (int k = 0; k < KT; ++k) { z[k] = -INFINITY; id[k] = -1; c[k] = 0.0f; }
         }
     }
+    __device__ __forceinline__ void bind(unsigned char *, int) {}
+    __device__ __forceinline__ double get_z(int k) const { return z[k]; }
+    __device__ __forceinline__ int get_id(int k) const { return id[k]; }
+    __device__ __forceinline__ float get_c(int k) const { return c[k]; }
     // keep the KT largest by (z desc, id asc) -- raster.py:389-399
     __device__ __forceinline__ void insert(double zz, int sid, float cl) {
         if (!(zz > z[KT - 1] || (zz == z[KT - 1] && sid < id[KT - 1]))) return;
@@ -78,6 +84,45 @@ struct TopK {
     }
 };
 
+// Shared-memory variant for K <= 8: the K x 256 record lives in shared memory (column tid), only the
+// current worst entry (the admission threshold) is cached in registers.  Frees ~17 registers per
+// thread, which lets a fourth CTA fit on each SM.
+template <int KT>
+struct TopKShared {
+    double *z; int *id; float *c;  // this thread's column: slot k at [k * TILE_PX]
+    double wz; int wid;            // cached slot KT-1
+    __device__ __forceinline__ void bind(unsigned char *base, int tid) {
+        z = (double *)base + tid;
+        id = (int *)(base + (size_t)KT * TILE_PX * 8) + tid;
+        c = (float *)(base + (size_t)KT * TILE_PX * 12) + tid;
+    }
+    __device__ __forceinline__ void init() {
+#pragma unroll
+        for (int k = 0; k < KT; ++k) { z[k * TILE_PX] = -INFINITY; id[k * TILE_PX] = -1; c[k * TILE_PX] = 0.0f; }
+        wz = -INFINITY; wid = -1;
+    }
+    __device__ __forceinline__ void insert(double zz, int sid, float cl) {
+        if (!(zz > wz || (zz == wz && sid < wid))) return;
+        int k = KT - 1;
+        while (k > 0) {
+            const double zk = z[(k - 1) * TILE_PX];
+            const int ik = id[(k - 1) * TILE_PX];
+            if (!(zz > zk || (zz == zk && sid < ik))) break;
+            z[k * TILE_PX] = zk; id[k * TILE_PX] = ik; c[k * TILE_PX] = c[(k - 1) * TILE_PX];
+            --k;
+        }
+        z[k * TILE_PX] = zz; id[k * TILE_PX] = sid; c[k * TILE_PX] = cl;
+        wz = z[(KT - 1) * TILE_PX]; wid = id[(KT - 1) * TILE_PX];
+    }
+    __device__ __forceinline__ double get_z(int k) const { return z[k * TILE_PX]; }
+    __device__ __forceinline__ int get_id(int k) const { return id[k * TILE_PX]; }
+    __device__ __forceinline__ float get_c(int k) const { return c[k * TILE_PX]; }
+};
+
+#ifndef SS_TOPK_SHARED
+#define SS_TOPK_SHARED 1  // K <= 8: top-K record in shared memory (1) or registers (0)
+#endif
+
 __device__ __forceinline__ float ex2_approx(float x) {
     float y;
     asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
@@ -97,7 +142,7 @@ __device__ __forceinline__ float pin_reg(float x) {
 
 constexpr float kLn2 = 0.6931471805599453f;
 #ifndef SS_RASTER_MINB
-#define SS_RASTER_MINB 3  // resident CTAs per SM the register allocation targets (d <= 4, K <= 8)
+#define SS_RASTER_MINB (SS_TOPK_SHARED ? 4 : 3)  // resident CTAs per SM the register allocation targets (d <= 4, K <= 8)
 #endif
 constexpr int DRAIN_MIN_ACTIVE = 12;
 
@@ -177,7 +222,9 @@ __global__ void __launch_bounds__(TILE_PX, (KT <= 8 && DP <= 4) ? SS_RASTER_MINB
     float num[DP];
 #pragma unroll
     for (int i = 0; i < DP; ++i) num[i] = 0.0f;
-    TopK<KT> top;
+    constexpr bool kTopShared = (SS_TOPK_SHARED != 0) && KT <= 8;
+    typename std::conditional<kTopShared, TopKShared<KT>, TopK<KT>>::type top;
+    top.bind(s_list + 8 * LSTRIDE, tid);  // shared variant: KT x 256 x 16 B behind the warp lists
     top.init();
     bool done = !valid;
     unsigned n_hits = 0;
@@ -342,19 +389,19 @@ __global__ void __launch_bounds__(TILE_PX, (KT <= 8 && DP <= 4) ? SS_RASTER_MINB
 #pragma unroll
                 for (int k = 0; k < KT; ++k) {
                     if (k < a.K) {
-                        const bool empty = top.id[k] < 0;
-                        a.ids[k * P + pix] = top.id[k];
-                        a.z[k * P + pix] = empty ? 0.0f : (float)top.z[k];
-                        a.clos[k * P + pix] = top.c[k];
+                        const int tid_k = top.get_id(k);
+                        a.ids[k * P + pix] = tid_k;
+                        a.z[k * P + pix] = tid_k < 0 ? 0.0f : (float)top.get_z(k);
+                        a.clos[k * P + pix] = top.get_c(k);
                     }
                 }
             } else {
 #pragma unroll 1
                 for (int k = 0; k < a.K; ++k) {
-                    const bool empty = top.id[k] < 0;
-                    a.ids[k * P + pix] = top.id[k];
-                    a.z[k * P + pix] = empty ? 0.0f : (float)top.z[k];
-                    a.clos[k * P + pix] = top.c[k];
+                    const int tid_k = top.get_id(k);
+                    a.ids[k * P + pix] = tid_k;
+                    a.z[k * P + pix] = tid_k < 0 ? 0.0f : (float)top.get_z(k);
+                    a.clos[k * P + pix] = top.get_c(k);
                 }
             }
             a.log_denom[pix] = ld2 * kLn2;
@@ -381,18 +428,25 @@ __global__ void __launch_bounds__(TILE_PX, (KT <= 8 && DP <= 4) ? SS_RASTER_MINB
     }
 }
 
-template <int DP>
+template <int DP, int KT>
 constexpr size_t raster_smem_bytes() {
-    return (size_t)SS_MAX_CHUNK * (16 + 16 + 32 + 4 * DP) + SS_MAX_CHUNK + 8 * (SS_MAX_CHUNK + 4);
+    return (size_t)SS_MAX_CHUNK * (16 + 16 + 32 + 4 * DP) + SS_MAX_CHUNK + 8 * (SS_MAX_CHUNK + 4) +
+           ((SS_TOPK_SHARED != 0 && KT <= 8) ? (size_t)KT * TILE_PX * 16 : 0);
 }
 
 template <int DP, int KT, int MODE>
 void launch_one(const RasterArgs &r, int n_tiles, cudaStream_t s) {
-    constexpr size_t smem = raster_smem_bytes<DP>();
+    constexpr size_t smem = raster_smem_bytes<DP, KT>();
     static bool attr_done = false;  // per instantiation
     if (!attr_done) {
         if (smem + 1024 > 48 * 1024)
             cudaFuncSetAttribute(k_raster<DP, KT, MODE>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+#ifndef SS_RASTER_CARVEOUT
+#define SS_RASTER_CARVEOUT -1  // percent of the unified L1/shared storage to prefer as shared; -1 = driver default
+#endif
+        if (SS_RASTER_CARVEOUT >= 0)
+            cudaFuncSetAttribute(k_raster<DP, KT, MODE>, cudaFuncAttributePreferredSharedMemoryCarveout,
+                                 SS_RASTER_CARVEOUT);
         attr_done = true;
     }
     k_raster<DP, KT, MODE><<<n_tiles, TILE_PX, smem, s>>>(r);

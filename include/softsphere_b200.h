@@ -200,6 +200,7 @@ int64_t ss_launch_count(void);
  * the device and returns, per kernel id, the summed duration in ms and the launch count since
  * the last enable/collect. */
 void ss_profile_enable(int on);
+void ss_profile_enable_mask(unsigned mask); /* bit k = time kernel id k only */
 int ss_profile_collect(double *ms_sum, int64_t *launches, int n);
 int ss_profile_kernel_count(void);
 const char *ss_profile_kernel_name(int kid);

@@ -76,7 +76,7 @@ class SsStatus(C.Structure):
 
 EXPORTS = ("ss_abi_version", "ss_status_string", "ss_last_cuda_error", "ss_workspace_bytes",
            "ss_forward", "ss_backward", "ss_read_status", "ss_debug_tile_lists", "ss_launch_count",
-           "ss_profile_enable", "ss_profile_collect", "ss_profile_kernel_count", "ss_profile_kernel_name")
+           "ss_profile_enable", "ss_profile_enable_mask", "ss_profile_collect", "ss_profile_kernel_count", "ss_profile_kernel_name")
 
 _lib = None
 
@@ -111,6 +111,8 @@ def load():
     lib.ss_launch_count.restype = C.c_int64
     lib.ss_profile_enable.restype = None
     lib.ss_profile_enable.argtypes = [C.c_int]
+    lib.ss_profile_enable_mask.restype = None
+    lib.ss_profile_enable_mask.argtypes = [C.c_uint]
     lib.ss_profile_collect.restype = C.c_int
     lib.ss_profile_collect.argtypes = [C.POINTER(C.c_double), C.POINTER(C.c_int64), C.c_int]
     lib.ss_profile_kernel_count.restype = C.c_int
@@ -136,6 +138,17 @@ def launch_count() -> int:
 
 def profile_enable(on: bool) -> None:
     load().ss_profile_enable(1 if on else 0)
+
+
+def profile_enable_only(names) -> None:
+    """Time only the named kernels (e.g. ['k_raster'])."""
+    lib = load()
+    n = lib.ss_profile_kernel_count()
+    mask = 0
+    for i in range(n):
+        if lib.ss_profile_kernel_name(i).decode() in names:
+            mask |= 1 << i
+    lib.ss_profile_enable_mask(mask)
 
 
 def profile_collect() -> dict:

@@ -13,13 +13,13 @@ static thread_local cudaError_t g_last_cuda = cudaSuccess;
 void count_launch(int n) { g_launches += n; }
 
 // ---- per-kernel event timing -------------------------------------------------------------
-static bool g_prof_on = false;
+static unsigned g_prof_mask = 0;  // bit k: time kernel id k
 static const int kProfCap = 8192;
 static cudaEvent_t g_ev0[kProfCap], g_ev1[kProfCap];
 static int g_ev_kid[kProfCap];
 static int g_ev_made = 0, g_ev_used = 0;
 void prof_begin(int kid, cudaStream_t s) {
-    if (!g_prof_on || g_ev_used >= kProfCap) return;
+    if (!((g_prof_mask >> kid) & 1u) || g_ev_used >= kProfCap) return;
     if (g_ev_used >= g_ev_made) {
         cudaEventCreate(&g_ev0[g_ev_made]);
         cudaEventCreate(&g_ev1[g_ev_made]);
@@ -29,8 +29,7 @@ void prof_begin(int kid, cudaStream_t s) {
     cudaEventRecord(g_ev0[g_ev_used], s);
 }
 void prof_end(int kid, cudaStream_t s) {
-    if (!g_prof_on || g_ev_used >= kProfCap) return;
-    (void)kid;
+    if (!((g_prof_mask >> kid) & 1u) || g_ev_used >= kProfCap) return;
     cudaEventRecord(g_ev1[g_ev_used], s);
     ++g_ev_used;
 }
@@ -102,7 +101,9 @@ const char *ss_last_cuda_error(void) { return cudaGetErrorString(ss::g_last_cuda
 
 int64_t ss_launch_count(void) { return (int64_t)ss::g_launches.load(); }
 
-void ss_profile_enable(int on) { ss::g_prof_on = on != 0; ss::g_ev_used = 0; }
+void ss_profile_enable(int on) { ss::g_prof_mask = on ? 0xffffffffu : 0u; ss::g_ev_used = 0; }
+
+void ss_profile_enable_mask(unsigned mask) { ss::g_prof_mask = mask; ss::g_ev_used = 0; }
 
 int ss_profile_collect(double *ms_sum, int64_t *launches, int n) {
     if (!ms_sum || !launches) return SS_ERR_NULL;

@@ -333,9 +333,13 @@ void launch_bw_mode(const BackArgs &b, int n_tiles, int mode, cudaStream_t s) {
 
 template <int DP>
 void launch_bw_k(const BackArgs &b, int n_tiles, int mode, cudaStream_t s) {
+#ifdef SS_EXPERIMENT_BWD_LOOP
+    launch_bw_mode<DP, 0>(b, n_tiles, mode, s);
+#else
     if (DP <= 4 && b.K <= 5) launch_bw_mode<DP, 5>(b, n_tiles, mode, s);
     else if (DP <= 4 && b.K <= 8) launch_bw_mode<DP, 8>(b, n_tiles, mode, s);
     else launch_bw_mode<DP, 0>(b, n_tiles, mode, s);
+#endif
 }
 
 }  // namespace

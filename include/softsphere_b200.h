@@ -180,6 +180,12 @@ const char *ss_last_cuda_error(void);
 /* Bytes of caller-owned device workspace for `dims` (256-byte aligned base required). */
 int ss_workspace_bytes(const SsDims *dims, size_t *out_bytes);
 
+/* Must be called once on a freshly allocated (or re-laid-out) workspace before its first use: clears
+ * the status block and the "gradient accumulators are clean" tag.  ss_backward re-zeroes only the
+ * accumulator rows it touched and trusts that tag on the next call (instead of a 48 MB memset per
+ * call at 1M spheres); a stale tag in recycled memory would be trusted wrongly. */
+int ss_workspace_init(const SsDims *dims, void *workspace, size_t workspace_bytes, void *stream);
+
 /* `stream` is a cudaStream_t passed as void* (NULL = default stream). */
 int ss_forward(const SsForwardArgs *args, void *stream);
 int ss_backward(const SsBackwardArgs *args, void *stream);

@@ -74,7 +74,7 @@ class SsStatus(C.Structure):
                 ("reserved", C.c_int64 * 9)]
 
 
-EXPORTS = ("ss_abi_version", "ss_status_string", "ss_last_cuda_error", "ss_workspace_bytes",
+EXPORTS = ("ss_abi_version", "ss_status_string", "ss_last_cuda_error", "ss_workspace_bytes", "ss_workspace_init",
            "ss_forward", "ss_backward", "ss_read_status", "ss_debug_tile_lists", "ss_launch_count",
            "ss_profile_enable", "ss_profile_enable_mask", "ss_profile_collect", "ss_profile_kernel_count", "ss_profile_kernel_name")
 
@@ -100,6 +100,8 @@ def load():
     lib.ss_last_cuda_error.restype = C.c_char_p
     lib.ss_workspace_bytes.restype = C.c_int
     lib.ss_workspace_bytes.argtypes = [C.POINTER(SsDims), C.POINTER(C.c_size_t)]
+    lib.ss_workspace_init.restype = C.c_int
+    lib.ss_workspace_init.argtypes = [C.POINTER(SsDims), C.c_void_p, C.c_size_t, C.c_void_p]
     lib.ss_forward.restype = C.c_int
     lib.ss_forward.argtypes = [C.POINTER(SsForwardArgs), C.c_void_p]
     lib.ss_backward.restype = C.c_int

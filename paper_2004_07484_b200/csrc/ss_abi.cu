@@ -137,6 +137,20 @@ int ss_workspace_bytes(const SsDims *dims, size_t *out_bytes) {
     return SS_OK;
 }
 
+int ss_workspace_init(const SsDims *dims, void *workspace, size_t workspace_bytes, void *stream) {
+    if (!dims || !workspace) return SS_ERR_NULL;
+    int rc = check_dims(*dims);
+    if (rc != SS_OK) return rc;
+    const Layout L = make_layout(*dims);
+    if (workspace_bytes < L.total) return SS_ERR_WORKSPACE;
+    cudaStream_t s = (cudaStream_t)stream;
+    cudaError_t e = cudaMemsetAsync((char *)workspace + L.status, 0, 16 * sizeof(int64_t), s);
+    if (e != cudaSuccess) return cuda_fail(e);
+    e = cudaMemsetAsync((char *)workspace + L.cam_part, 0, (CAM_VALS + 2) * sizeof(double), s);
+    if (e != cudaSuccess) return cuda_fail(e);
+    return SS_OK;
+}
+
 int ss_forward(const SsForwardArgs *a, void *stream) {
     if (!a) return SS_ERR_NULL;
     int rc = check_dims(a->dims);

@@ -24,6 +24,7 @@ struct BackArgs {
     const float *feat, *bg;
     const int *ids; const float *z, *clos, *log_denom, *upstream;
     float *raw; int raw_stride;
+    unsigned long long *clean_tag;
     int d, K;
     double gamma, eps_over_g;
 };
@@ -122,6 +123,7 @@ __global__ void __launch_bounds__(TILE_PX, (KT > 0) ? SS_BACKWARD_MINB : 1) k_ba
     const Cam &cam = a.cam;
     const int tile = blockIdx.x;
     const int tid = threadIdx.x;
+    if (tile == 0 && tid == 0) *a.clean_tag = 0ull;  // accumulators are being written: not clean any more
     const int lane = tid & 31, warp = tid >> 5;
     const int px = (tile % cam.ntx) * TILE + (((warp & 1) << 3) | (lane & 7));  // 8x4 block per warp
     const int py = (tile / cam.ntx) * TILE + (((warp >> 1) << 2) | (lane >> 3));
@@ -220,67 +222,100 @@ __global__ void __launch_bounds__(TILE_PX, (KT > 0) ? SS_BACKWARD_MINB : 1) k_ba
     }
 }
 
+// ---- clean-accumulator protocol ---------------------------------------------------------------
+// The raw accumulator rows (M x raw_stride floats, 48 MB at C3) must be zero when k_backward starts.
+// Instead of a memset per call, k_finalize re-zeroes exactly the rows it consumed (the ~1/3 of the
+// spheres that were touched) and then stamps the workspace with a tag derived from the layout;
+// k_raw_prepare zeroes everything only when the tag is missing (first call, new layout, aborted call).
+// A fresh workspace must not carry a stale tag: ss_forward clears it, and the tag also encodes dims.
+constexpr int BST_COUNTER = CAM_VALS;      // cam_part[16]: completion counter (as unsigned)
+constexpr int BST_TAG = CAM_VALS + 1;      // cam_part[17]: clean tag (as unsigned long long)
+
+__global__ void __launch_bounds__(256) k_raw_prepare(float4 *raw4, size_t n4, double *bst, unsigned long long tag) {
+    const bool clean = ((const unsigned long long *)bst)[BST_TAG] == tag;
+    if (blockIdx.x == 0 && threadIdx.x <= CAM_VALS) bst[threadIdx.x] = 0.0;  // camera sums + counter
+    if (clean) return;
+    const float4 z = make_float4(0.f, 0.f, 0.f, 0.f);
+    for (size_t i = (size_t)blockIdx.x * blockDim.x + threadIdx.x; i < n4; i += (size_t)gridDim.x * blockDim.x)
+        raw4[i] = z;
+}
+
 struct FinArgs {
     long long M; int d, raw_stride;
     Cam cam;
     const float *pos;
-    const float *raw;
+    float *raw;
     const double *proj_r;
     float *d_pos, *d_rad, *d_opa, *d_feat; int *pixel_count;
     double *cam_part; double *cam_grad;
+    unsigned long long tag;
     int normalize, gate, cam_grads, accumulate;
 };
 
+// One thread per sphere.  The kernel is instruction-bound, not bandwidth-bound (ncu: a staged,
+// "coalesced" variant executed 950 instructions per warp and took 58 us), so this version keeps the
+// per-thread path short: three 128-bit row loads, float32 per-sphere math (the accumulators are float32
+// sums already), float64 only for the 14 camera sums, which are reduced through a shared-memory
+// transpose instead of 14 x 5 double shuffles.
 __global__ void __launch_bounds__(256) k_finalize(FinArgs a) {
-    __shared__ double s_part[8][CAM_VALS];
-    __shared__ int s_last;
+    __shared__ double s_red[14][8];
     const Cam &cam = a.cam;
-    const double *R = cam.R;
-    double acc[14];
+    const int RS = a.raw_stride, d = a.d;
+    const int t = threadIdx.x;
+    const long long i = (long long)blockIdx.x * 256 + t;
+    bool touched = false;
+    float acc[14];
 #pragma unroll
-    for (int j = 0; j < 14; ++j) acc[j] = 0.0;
-    const long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+    for (int j = 0; j < 14; ++j) acc[j] = 0.0f;
     if (i < a.M) {
-        const float4 *row = (const float4 *)(a.raw + (size_t)i * a.raw_stride);
+        float4 *row = (float4 *)(a.raw + (size_t)i * RS);
         const float4 r0 = row[0], r1 = row[1];
         const float cnt = r1.w;
-        float dp0 = 0.f, dp1 = 0.f, dp2 = 0.f, drad = 0.f, dopa = 0.f;
-        if (cnt > 0.0f) {
-            double div = 1.0, cam_scale = 1.0;
+        touched = cnt > 0.0f;
+        float dp0 = 0.f, dp1 = 0.f, dp2 = 0.f, drad = 0.f, dopa = 0.f, inv_div = 0.f;
+        if (touched) {
             const double pr = a.proj_r[i];
+            float cam_scale = 1.0f;
+            inv_div = 1.0f;
             if (a.normalize) {
-                div = (double)cnt;
-                cam_scale = 1e-3 / fmax(3.14159265358979323846 * (pr * pr), 1.0);
+                inv_div = 1.0f / cnt;
+                cam_scale = 1e-3f / fmaxf(3.14159265358979f * (float)(pr * pr), 1.0f);
             }
-            const double gx = r0.x, gy = r0.y, gz = r0.z;
-            const double inv_div = 1.0 / div;
-            dp0 = (float)((gx * R[0] + gy * R[3] + gz * R[6]) * inv_div);
-            dp1 = (float)((gx * R[1] + gy * R[4] + gz * R[7]) * inv_div);
-            dp2 = (float)((gx * R[2] + gy * R[5] + gz * R[8]) * inv_div);
-            drad = (float)((double)r0.w * inv_div);
-            dopa = (float)((double)r1.x * inv_div);
+            const float R0 = (float)cam.R[0], R1 = (float)cam.R[1], R2 = (float)cam.R[2], R3 = (float)cam.R[3],
+                        R4 = (float)cam.R[4], R5 = (float)cam.R[5], R6 = (float)cam.R[6], R7 = (float)cam.R[7],
+                        R8 = (float)cam.R[8];
+            dp0 = (r0.x * R0 + r0.y * R3 + r0.z * R6) * inv_div;  // d_position = (g_center @ R) / count
+            dp1 = (r0.x * R1 + r0.y * R4 + r0.z * R7) * inv_div;
+            dp2 = (r0.x * R2 + r0.y * R5 + r0.z * R8) * inv_div;
+            drad = r0.w * inv_div;
+            dopa = r1.x * inv_div;
             if (a.gate && pr <= 3.0) { dp0 = dp1 = dp2 = 0.f; drad = 0.f; }  // grad.py:305-320
-            const float *fr = a.raw + (size_t)i * a.raw_stride + 8;
-            for (int k = 0; k < a.d; ++k) {
-                float v = (float)((double)fr[k] * inv_div);
-                if (a.accumulate) a.d_feat[(size_t)i * a.d + k] += v; else a.d_feat[(size_t)i * a.d + k] = v;
-            }
             if (a.cam_grads) {
-                const double sx = cam_scale * gx, sy = cam_scale * gy, sz = cam_scale * gz;
-                const double rx = (double)a.pos[3 * i] - cam.t[0], ry = (double)a.pos[3 * i + 1] - cam.t[1],
-                             rz = (double)a.pos[3 * i + 2] - cam.t[2];
+                const float sx = cam_scale * r0.x, sy = cam_scale * r0.y, sz = cam_scale * r0.z;
+                const float rx = (float)((double)a.pos[3 * i] - cam.t[0]), ry = (float)((double)a.pos[3 * i + 1] - cam.t[1]),
+                            rz = (float)((double)a.pos[3 * i + 2] - cam.t[2]);
                 acc[0] = sx; acc[1] = sy; acc[2] = sz;
                 acc[3] = sx * rx; acc[4] = sx * ry; acc[5] = sx * rz;
                 acc[6] = sy * rx; acc[7] = sy * ry; acc[8] = sy * rz;
                 acc[9] = sz * rx; acc[10] = sz * ry; acc[11] = sz * rz;
-                acc[12] = cam_scale * (double)r1.y;
-                acc[13] = cam_scale * (double)r1.z;
+                acc[12] = cam_scale * r1.y;
+                acc[13] = cam_scale * r1.z;
             }
-        } else if (!a.accumulate) {
-            for (int k = 0; k < a.d; ++k) a.d_feat[(size_t)i * a.d + k] = 0.0f;
+        }
+        // features: RS - 8 = ceil4(d) floats behind the two fixed quads
+        float *df = a.d_feat + (size_t)i * d;
+        for (int q = 0; q * 4 < d; ++q) {
+            float4 f4 = touched ? row[2 + q] : make_float4(0.f, 0.f, 0.f, 0.f);
+            const float v[4] = {f4.x * inv_div, f4.y * inv_div, f4.z * inv_div, f4.w * inv_div};
+#pragma unroll
+            for (int c = 0; c < 4; ++c)
+                if (q * 4 + c < d) {
+                    if (a.accumulate) { if (touched) df[q * 4 + c] += v[c]; }
+                    else df[q * 4 + c] = v[c];
+                }
         }
         if (a.accumulate) {
-            if (cnt > 0.0f) {
+            if (touched) {
                 a.d_pos[3 * i] += dp0; a.d_pos[3 * i + 1] += dp1; a.d_pos[3 * i + 2] += dp2;
                 a.d_rad[i] += drad; a.d_opa[i] += dopa; a.pixel_count[i] += (int)cnt;
             }
@@ -288,34 +323,46 @@ __global__ void __launch_bounds__(256) k_finalize(FinArgs a) {
             a.d_pos[3 * i] = dp0; a.d_pos[3 * i + 1] = dp1; a.d_pos[3 * i + 2] = dp2;
             a.d_rad[i] = drad; a.d_opa[i] = dopa; a.pixel_count[i] = (int)cnt;
         }
+        if (touched) {  // give the row back clean for the next call
+            const float4 z = make_float4(0.f, 0.f, 0.f, 0.f);
+            for (int q = 0; q < RS / 4; ++q) row[q] = z;
+        }
     }
-    if (!a.cam_grads) return;
-    // block reduction of the 14 camera sums (float64), one double atomic per value and block into the
-    // global accumulators, then the last block to finish converts the sums into the camera block
-    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+
+    // camera sums: float32 butterfly inside the warp (32 terms), float64 from there on: per-warp
+    // partials in shared memory, ONE block barrier, then warp 0 alone adds the block's 14 sums to the
+    // global accumulators (double atomics), fences and bumps the completion counter; the last block
+    // publishes the camera block and the clean tag.
+    const int lane = t & 31, wid = t >> 5;
+    if (a.cam_grads && __any_sync(0xffffffffu, touched)) {
 #pragma unroll
-    for (int j = 0; j < 14; ++j) {
-        double v = acc[j];
-        for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
-        if (lane == 0) s_part[wid][j] = v;
+        for (int j = 0; j < 14; ++j) {
+            float v = acc[j];
+            for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+            if (lane == 0) s_red[j][wid] = (double)v;
+        }
+    } else if (lane == 0) {
+#pragma unroll
+        for (int j = 0; j < 14; ++j) s_red[j][wid] = 0.0;
     }
     __syncthreads();
-    double *sums = a.cam_part;  // 16 doubles, zeroed by launch_backward
-    if (threadIdx.x < 14) {
+    if (wid != 0) return;
+    if (a.cam_grads && lane < 14) {
         double v = 0.0;
-        for (int w = 0; w < 8; ++w) v += s_part[w][threadIdx.x];
-        if (v != 0.0) atomicAdd(&sums[threadIdx.x], v);
+#pragma unroll
+        for (int e = 0; e < 8; ++e) v += s_red[lane][e];
+        if (v != 0.0) atomicAdd(&a.cam_part[lane], v);
     }
+    __syncwarp();
+    if (lane != 0) return;
+    __threadfence();  // orders this block's atomics (cumulative over the warp) before the counter
+    unsigned int *counter = (unsigned int *)(a.cam_part + BST_COUNTER);
+    if (atomicAdd(counter, 1u) != gridDim.x - 1) return;
     __threadfence();
-    __syncthreads();
-    unsigned int *counter = (unsigned int *)(a.cam_part + CAM_VALS);
-    if (threadIdx.x == 0) s_last = (atomicAdd(counter, 1u) == gridDim.x - 1);
-    __syncthreads();
-    if (!s_last) return;
-    __threadfence();
-    if (threadIdx.x == 0) {
-        volatile double *vs = sums;
-        double t0 = vs[0], t1 = vs[1], t2 = vs[2];
+    if (a.cam_grads) {
+        const double *R = cam.R;
+        volatile double *vs = a.cam_part;
+        const double t0 = vs[0], t1 = vs[1], t2 = vs[2];
         for (int j = 0; j < 3; ++j)  // d_translation = -(sum sc) @ R  (grad.py:289)
             a.cam_grad[j] = -(t0 * R[0 + j] + t1 * R[3 + j] + t2 * R[6 + j]);
         for (int j = 0; j < 9; ++j) a.cam_grad[3 + j] = vs[3 + j];
@@ -323,6 +370,7 @@ __global__ void __launch_bounds__(256) k_finalize(FinArgs a) {
         a.cam_grad[13] = vs[13];
         a.cam_grad[14] = 0.0; a.cam_grad[15] = 0.0;
     }
+    ((unsigned long long *)a.cam_part)[BST_TAG] = a.tag;  // every consumed row is zero again
 }
 
 template <int DP, int KT>
@@ -353,13 +401,16 @@ cudaError_t launch_backward(const BwdLaunch &a, cudaStream_t s) {
         return cudaSuccess;
     }
     float *raw = (float *)(a.ws + L.raw);
-    cudaError_t e;
+    double *bst = (double *)(a.ws + L.cam_part);
+    // tag of a clean accumulator region for exactly this layout
+    unsigned long long tag = 0x5353424b434c4e31ull;  // "SSBKCLN1"
+    tag ^= (unsigned long long)M * 0x9e3779b97f4a7c15ull;
+    tag ^= ((unsigned long long)L.raw_stride << 48) ^ ((unsigned long long)L.raw << 8) ^ (unsigned long long)a.dims.max_pairs;
     {
         ProfScope ps(KID_MEMSET_BWD, s);
-        e = cudaMemsetAsync(raw, 0, (size_t)M * L.raw_stride * sizeof(float), s);
-        if (e != cudaSuccess) return e;
-        e = cudaMemsetAsync(a.ws + L.cam_part, 0, (CAM_VALS + 2) * 8, s);  // camera sums + completion counter
-        if (e != cudaSuccess) return e;
+        const size_t n4 = (size_t)M * L.raw_stride / 4;
+        k_raw_prepare<<<148 * 8, 256, 0, s>>>((float4 *)raw, n4, bst, tag);
+        count_launch();
     }
     BackArgs b;
     b.cam = a.cam;
@@ -367,6 +418,7 @@ cudaError_t launch_backward(const BwdLaunch &a, cudaStream_t s) {
     b.feat = a.feat; b.bg = a.bg;
     b.ids = a.ids; b.z = a.z; b.clos = a.clos; b.log_denom = a.log_denom; b.upstream = a.upstream;
     b.raw = raw; b.raw_stride = L.raw_stride;
+    b.clean_tag = (unsigned long long *)bst + BST_TAG;
     b.d = a.dims.feature_dim; b.K = a.dims.top_k;
     b.gamma = a.gamma; b.eps_over_g = a.blend.eps / a.gamma;
     const int d = b.d, mode = a.cam.mode;
@@ -383,8 +435,9 @@ cudaError_t launch_backward(const BwdLaunch &a, cudaStream_t s) {
     f.proj_r = (const double *)(a.ws + L.proj_r);
     f.d_pos = a.d_pos; f.d_rad = a.d_rad; f.d_opa = a.d_opa; f.d_feat = a.d_feat;
     f.pixel_count = a.pixel_count;
-    f.cam_part = (double *)(a.ws + L.cam_part);
+    f.cam_part = bst;
     f.cam_grad = a.cam_grad;
+    f.tag = tag;
     f.normalize = (a.blend.flags & SS_OPT_NORMALIZE) ? 1 : 0;
     f.gate = (a.blend.flags & SS_OPT_GATE) ? 1 : 0;
     f.cam_grads = cam_grads ? 1 : 0;

@@ -144,7 +144,10 @@ constexpr float kLn2 = 0.6931471805599453f;
 #ifndef SS_RASTER_MINB
 #define SS_RASTER_MINB (SS_TOPK_SHARED ? 4 : 3)  // resident CTAs per SM the register allocation targets (d <= 4, K <= 8)
 #endif
-constexpr int DRAIN_MIN_ACTIVE = 12;
+#ifndef SS_DRAIN_MIN_ACTIVE
+#define SS_DRAIN_MIN_ACTIVE 12
+#endif
+constexpr int DRAIN_MIN_ACTIVE = SS_DRAIN_MIN_ACTIVE;
 
 template <int DP, int KT, int MODE>
 __global__ void __launch_bounds__(TILE_PX, (KT <= 8 && DP <= 4) ? SS_RASTER_MINB : 1) k_raster(RasterArgs a) {

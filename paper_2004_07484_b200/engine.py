@@ -112,6 +112,10 @@ class RenderEngine:
             _raise_for(rc)
         if self._ws is None or self._ws.numel() < nbytes.value:
             self._ws = torch.empty(nbytes.value, dtype=torch.uint8, device=self.device)
+        # a (re)laid-out workspace must not carry a stale "accumulators are clean" tag (ss_workspace_init)
+        rc = self.lib.ss_workspace_init(C.byref(dims), _ptr(self._ws), self._ws.numel(), self._stream())
+        if rc != _lib.SS_OK:
+            _raise_for(rc)
         self._ws_dims = key
         self._pair_capacity = cap
         self._last_fwd_key = None

@@ -35,7 +35,8 @@ def main():
     eng = RenderEngine("cuda")
     dev = [torch.from_numpy(x).cuda() for x in (pos, rad, opa, feat, bg)]
     f = eng.forward(*dev, spec, gamma=0.1, tau=a.tau, top_k=a.k, collect_stats=True)
-    print("status", f["status"], "workspace MB", eng._ws.numel() / 1e6)
+    status = f["status"]
+    print("status", status, "workspace MB", eng._ws.numel() / 1e6)
     up = torch.sign(f["image"] - 0.5)
     out = eng.backward(*dev, spec, f, up, gamma=0.1, eps=1e-2)
     torch.cuda.synchronize()
@@ -71,8 +72,8 @@ def main():
         img = f["image"].cpu().numpy().astype(np.float64)
         err = np.abs(img - ref["image"])
         print("image max abs err %.3e, max rel err %.3e" % (err.max(), (err / np.maximum(np.abs(ref["image"]), 1e-2)).max()))
-        print("stats equal:", f["status"]["hits_blended"] == ref["stats"]["hits_blended"],
-              f["status"]["candidates_tested"] == ref["stats"]["candidates_tested"])
+        print("stats equal:", status["hits_blended"] == ref["stats"]["hits_blended"],
+              status["candidates_tested"] == ref["stats"]["candidates_tested"])
         print("pixel_count equal:", bool(np.array_equal(out["pixel_count"].cpu().numpy(), gr["pixel_count"])))
         for name, key in (("d_pos", "d_position"), ("d_rad", "d_radius"), ("d_opa", "d_opacity"), ("d_feat", "d_feature")):
             g = out[name].cpu().numpy().astype(np.float64)

@@ -29,6 +29,22 @@ struct BackArgs {
     double gamma, eps_over_g;
 };
 
+__device__ __forceinline__ float rcp_approx(float x) {
+    float y;
+    asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+    return y;
+}
+__device__ __forceinline__ float sqrt_approx_f(float x) {
+    float y;
+    asm("sqrt.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+    return y;
+}
+__device__ __forceinline__ float ex2_approx_f(float x) {
+    float y;
+    asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+    return y;
+}
+
 __device__ __forceinline__ void red_add_v4(float *addr, float a, float b, float c, float d) {
 #ifdef SS_EXPERIMENT_NO_RED  // measurement only: floor of the kernel without the reductions
     if (a == 123456.f) *addr = b + c + d;
@@ -41,14 +57,13 @@ __device__ __forceinline__ void red_add_v4(float *addr, float a, float b, float 
 // Per-hit gradient pieces for one stored slot (grad.py:110-179); accumulates into the sphere's row.
 template <int DP, int MODE>
 __device__ __forceinline__ void slot_gradient(const BackArgs &a, const Rec &rc, int id, float zk, float ck,
-                                              float ld, float inv_g, const float *up, const float *fhat,
+                                              float E, float inv_g, const float *up, const float *fhat,
                                               const float *f, int d, double xs, double ys, double ux, double uy,
                                               double uz, double inv_vnorm) {
     const Cam &cam = a.cam;
     const float o = rc.o;
     const float ez = o * zk * inv_g;
-    const float E = expf(ez - ld);
-    const float w = o * ck * E;
+    const float w = o * ck * E;  // E = exp(o z / gamma - log_denom), computed once per slot by the caller
     float acoef = 0.0f;
 #pragma unroll
     for (int i = 0; i < DP; ++i)
@@ -65,18 +80,18 @@ __device__ __forceinline__ void slot_gradient(const BackArgs &a, const Rec &rc, 
         const double td = rc.cx * ux + rc.cy * uy + rc.cz * uz;
         const double ddx = rc.cx - td * ux, ddy = rc.cy - td * uy, ddz = rc.cz - td * uz;
         t = (float)td; dvx = (float)ddx; dvy = (float)ddy; dvz = (float)ddz;
-        dist = sqrtf((float)(ddx * ddx + ddy * ddy + ddz * ddz));
+        dist = sqrt_approx_f((float)(ddx * ddx + ddy * ddy + ddz * ddz));
     } else {
         const double ddx = rc.cx - xs, ddy = rc.cy - ys;
         t = (float)rc.cz; dvx = (float)ddx; dvy = (float)ddy; dvz = 0.0f;
-        dist = sqrtf((float)(ddx * ddx + ddy * ddy));
+        dist = sqrt_approx_f((float)(ddx * ddx + ddy * ddy));
     }
     const bool interior = (0.0f < zk) && (zk < 1.0f);
     const float dl_dzeta = interior ? -dl_dz * (float)cam.inv_range : 0.0f;
-    const float inv_r = 1.0f / r;
+    const float inv_r = rcp_approx(r);
     const float dl_ddist = -dl_dc * inv_r;
     const float d_radius = dl_dc * dist * inv_r * inv_r;
-    const float inv_dist = dist > 1e-12f ? 1.0f / dist : 0.0f;
+    const float inv_dist = dist > 1e-12f ? rcp_approx(dist) : 0.0f;
     const float hx = dvx * inv_dist, hy = dvy * inv_dist, hz = dvz * inv_dist;
     const float xsf = (float)xs, ysf = (float)ys;
     float gcx, gcy, gcz, g_focal, g_sensor;
@@ -95,10 +110,10 @@ __device__ __forceinline__ void slot_gradient(const BackArgs &a, const Rec &rc, 
         const float prz = fmaf(s1, dvz, zt * (1.0f - uzf * uzf));
         const float ivn = (float)inv_vnorm;
         g_focal = prz * ivn;
-        g_sensor = (prx * xsf + pry * ysf) * ivn / (float)cam.sensor_w;
+        g_sensor = (prx * xsf + pry * ysf) * ivn * (float)(1.0 / cam.sensor_w);
     } else {
         gcx = dl_ddist * hx; gcy = dl_ddist * hy; gcz = dl_ddist * hz + dl_dzeta;
-        g_sensor = -(dl_ddist * inv_dist) * (dvx * xsf + dvy * ysf) / (float)cam.sensor_w;
+        g_sensor = -(dl_ddist * inv_dist) * (dvx * xsf + dvy * ysf) * (float)(1.0 / cam.sensor_w);
         g_focal = 0.0f;
     }
     float *row = a.raw + (size_t)id * a.raw_stride;
@@ -157,7 +172,7 @@ __global__ void __launch_bounds__(TILE_PX, (KT > 0) ? SS_BACKWARD_MINB : 1) k_ba
     const float ld = a.log_denom[pix];
     const float inv_g = (float)(1.0 / a.gamma);
     float up[DP], fhat[DP];
-    const float w_bg = expf((float)a.eps_over_g - ld);
+    const float w_bg = ex2_approx_f(((float)a.eps_over_g - ld) * 1.4426950408889634f);
 #pragma unroll
     for (int i = 0; i < DP; ++i) {
         up[i] = i < d ? a.upstream[pix * d + i] : 0.0f;
@@ -183,11 +198,13 @@ __global__ void __launch_bounds__(TILE_PX, (KT > 0) ? SS_BACKWARD_MINB : 1) k_ba
 #pragma unroll
             for (int i = 0; i < DP; ++i) f[k][i] = (sid[k] >= 0 && i < d) ? a.feat[(size_t)id * d + i] : 0.0f;
         }
+        float Ek[KR];
 #pragma unroll
         for (int k = 0; k < KR; ++k) {
+            Ek[k] = 0.0f;
             if (sid[k] >= 0) {
-                const float E = expf(rc[k].o * zk[k] * inv_g - ld);
-                const float w = rc[k].o * ck[k] * E;
+                Ek[k] = ex2_approx_f((rc[k].o * zk[k] * inv_g - ld) * 1.4426950408889634f);
+                const float w = rc[k].o * ck[k] * Ek[k];
 #pragma unroll
                 for (int i = 0; i < DP; ++i) fhat[i] = fmaf(w, f[k][i], fhat[i]);
             }
@@ -195,14 +212,14 @@ __global__ void __launch_bounds__(TILE_PX, (KT > 0) ? SS_BACKWARD_MINB : 1) k_ba
 #pragma unroll
         for (int k = 0; k < KR; ++k)
             if (sid[k] >= 0)
-                slot_gradient<DP, MODE>(a, rc[k], sid[k], zk[k], ck[k], ld, inv_g, up, fhat, f[k], d, xs, ys, ux, uy,
-                                        uz, inv_vnorm);
+                slot_gradient<DP, MODE>(a, rc[k], sid[k], zk[k], ck[k], Ek[k], inv_g, up, fhat, f[k], d, xs, ys, ux,
+                                        uy, uz, inv_vnorm);
     } else {
         for (int k = 0; k < K; ++k) {
             const int id = ids[k * P + pix];
             if (id < 0) continue;
             const float o = a.rec[id].o;
-            const float E = expf(o * zb[k * P + pix] * inv_g - ld);
+            const float E = ex2_approx_f((o * zb[k * P + pix] * inv_g - ld) * 1.4426950408889634f);
             const float w = o * cb[k * P + pix] * E;
             const float *f = a.feat + (size_t)id * d;
 #pragma unroll
@@ -216,8 +233,10 @@ __global__ void __launch_bounds__(TILE_PX, (KT > 0) ? SS_BACKWARD_MINB : 1) k_ba
             float f[DP];
 #pragma unroll
             for (int i = 0; i < DP; ++i) f[i] = i < d ? a.feat[(size_t)id * d + i] : 0.0f;
-            slot_gradient<DP, MODE>(a, rc, id, zb[k * P + pix], cb[k * P + pix], ld, inv_g, up, fhat, f, d, xs, ys,
-                                    ux, uy, uz, inv_vnorm);
+            const float zk1 = zb[k * P + pix];
+            const float E1 = ex2_approx_f((rc.o * zk1 * inv_g - ld) * 1.4426950408889634f);
+            slot_gradient<DP, MODE>(a, rc, id, zk1, cb[k * P + pix], E1, inv_g, up, fhat, f, d, xs, ys, ux, uy, uz,
+                                    inv_vnorm);
         }
     }
 }

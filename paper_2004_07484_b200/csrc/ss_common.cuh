@@ -25,6 +25,7 @@ struct Cam {
     double ppu;        // W / sensor_w (pixels per metric unit)
     double pix;        // sensor_w / W
     double inv_range;  // 1 / (far - near)
+    double inv_f_ppu;  // 1 / (focal * ppu)
     int W, H, mode;
     int ntx, nty;
 };
@@ -100,6 +101,7 @@ inline Cam make_cam(const SsCamera &c) {
     k.ppu = (double)c.width / c.sensor_w;
     k.pix = c.sensor_w / (double)c.width;
     k.inv_range = 1.0 / (c.far_ - c.near_);
+    k.inv_f_ppu = 1.0 / (c.focal * k.ppu);
     k.W = c.width; k.H = c.height; k.mode = c.mode;
     k.ntx = (c.width + TILE - 1) / TILE;
     k.nty = (c.height + TILE - 1) / TILE;

@@ -30,17 +30,21 @@ __device__ __forceinline__ double clampd(double x, double lo, double hi) {
 }
 
 // raster.py:130-154
-__device__ void axis_extent_pinhole(double ca, double cz, double r, double focal, double &lo,
+__device__ void axis_extent_pinhole(double ca, double cz, double inv_cz, double r, double focal, double &lo,
                                     double &hi, bool &empty) {
     double n2 = ca * ca + cz * cz;
     if (cz > r * 1.000001 && n2 > r * r) {
         // Disc strictly in front of the camera plane: |phi| + beta < pi/2, so the wedge neither crosses
-        // the horizon nor is empty or full, and tan(phi -+ beta) has the closed form below (same value
-        // as the reference's asin/atan2/tan chain to a few ulp, at a third of the FP64 instructions).
-        const double tb = r / sqrt(n2 - r * r);  // tan(beta), beta = asin(r / n)
-        const double tp = ca / cz;               // tan(phi), phi = atan2(ca, cz)
-        lo = focal * ((tp - tb) / (1.0 + tp * tb));
-        hi = focal * ((tp + tb) / (1.0 - tp * tb));
+        // the horizon nor is empty or full, and tan(phi -+ beta) has a closed form (same value as the
+        // reference's asin/atan2/tan chain to a few ulp).  One rsqrt and one reciprocal per axis:
+        // tan(phi - beta) = (tp - tb)(1 - tp tb) / D, tan(phi + beta) = (tp + tb)(1 + tp tb) / D,
+        // D = 1 - (tp tb)^2 > 0.
+        const double tb = r * rsqrt(n2 - r * r);  // tan(beta), beta = asin(r / n)
+        const double tp = ca * inv_cz;            // tan(phi), phi = atan2(ca, cz)
+        const double pq = tp * tb;
+        const double inv_d = focal / (1.0 - pq * pq);
+        lo = (tp - tb) * (1.0 - pq) * inv_d;
+        hi = (tp + tb) * (1.0 + pq) * inv_d;
         empty = false;
         return;
     }
@@ -57,14 +61,16 @@ __device__ void axis_extent_pinhole(double ca, double cz, double r, double focal
 }
 
 // raster.py:157-178
-__device__ void discretize_extent(double lo_px, double hi_px, double center_px, int limit, int &i_lo,
-                                  int &i_hi, bool &outside) {
+template <typename CenterFn>
+__device__ __forceinline__ void discretize_extent(double lo_px, double hi_px, CenterFn center_px_fn, int limit,
+                                                  int &i_lo, int &i_hi, bool &outside) {
     double pad = 1e-9 * (1.0 + fabs(lo_px));
     double lo_f = clampd(ceil(lo_px - 0.5 - pad), -kIntHuge, kIntHuge);
     pad = 1e-9 * (1.0 + fabs(hi_px));
     double hi_f = clampd(floor(hi_px - 0.5 + pad), -kIntHuge, kIntHuge);
     long long a = (long long)lo_f, b = (long long)hi_f;
-    if (a > b) {
+    if (a > b) {  // sub-pixel extent: the pixel containing the projected centre (rare; exact division here)
+        const double center_px = center_px_fn();
         double c = isfinite(center_px) ? center_px : 0.0;
         long long nearest = (long long)clampd(floor(c), -kIntHuge, kIntHuge);
         a = nearest; b = nearest;
@@ -121,46 +127,85 @@ __global__ void __launch_bounds__(256) k_project(ProjectArgs a) {
         Rec rc; rc.cx = cx; rc.cy = cy; rc.cz = cz; rc.r = rf; rc.o = fminf(fmaxf(of, 0.0f), 1.0f);
         a.rec[i] = rc;
 
-        double lo_x, hi_x, lo_y, hi_y, u_c, v_c, e, pr;
+        double lo_x, hi_x, lo_y, hi_y;
         bool empty_x = false, empty_y = false;
-        bool behind = (cz + r) <= 0.0;
-        int w = cam.W, h = cam.H;
-        if (cam.mode == SS_MODE_PINHOLE) {
-            axis_extent_pinhole(cx, cz, r, cam.focal, lo_x, hi_x, empty_x);
-            axis_extent_pinhole(cy, cz, r, cam.focal, lo_y, hi_y, empty_y);
-            double safe_z = cz > 0.0 ? cz : INFINITY;
-            u_c = w / 2.0 + cam.focal * cx / safe_z * cam.ppu;
-            v_c = h / 2.0 + cam.focal * cy / safe_z * cam.ppu;
-            double d2 = cx * cx + cy * cy + cz * cz;
+        const bool behind = (cz + r) <= 0.0;
+        const bool pin = cam.mode == SS_MODE_PINHOLE;
+        const int w = cam.W, h = cam.H;
+        const double inv_cz = cz > 0.0 ? 1.0 / cz : 0.0;  // fast paths only (never feeds an exact quantity)
+        if (pin) {
+            axis_extent_pinhole(cx, cz, inv_cz, r, cam.focal, lo_x, hi_x, empty_x);
+            axis_extent_pinhole(cy, cz, inv_cz, r, cam.focal, lo_y, hi_y, empty_y);
+        } else {
+            lo_x = cx - r; hi_x = cx + r; lo_y = cy - r; hi_y = cy + r;
+        }
+        // rectangle, visibility and the histogram atomics come first: the slot indices they return are
+        // only needed at the very end, so their latency hides behind the rest of the per-sphere math
+        ushort4 tr = make_ushort4(1, 0, 1, 0);
+        int sl[4] = {0, 0, 0, 0};
+        int nt = 0;
+        if (!a.records_only) {
+            int x0, x1, y0, y1; bool out_x, out_y;
+            const double safe_z = cz > 0.0 ? cz : INFINITY;
+            auto u_c = [&]() { return pin ? w / 2.0 + cam.focal * cx / safe_z * cam.ppu : w / 2.0 + cx * cam.ppu; };
+            auto v_c = [&]() { return pin ? h / 2.0 + cam.focal * cy / safe_z * cam.ppu : h / 2.0 + cy * cam.ppu; };
+            discretize_extent(w / 2.0 + lo_x * cam.ppu, w / 2.0 + hi_x * cam.ppu, u_c, w, x0, x1, out_x);
+            discretize_extent(h / 2.0 + lo_y * cam.ppu, h / 2.0 + hi_y * cam.ppu, v_c, h, y0, y1, out_y);
+            on = !(behind || empty_x || empty_y || out_x || out_y) && !bad;
+            if (a.rect) {
+                a.rect[4 * i] = x0; a.rect[4 * i + 1] = x1; a.rect[4 * i + 2] = y0; a.rect[4 * i + 3] = y1;
+            }
+            if (a.on_sensor) a.on_sensor[i] = on ? 1 : 0;
+            if (on) {
+                tr.x = (unsigned short)(x0 / TILE); tr.y = (unsigned short)(x1 / TILE);
+                tr.z = (unsigned short)(y0 / TILE); tr.w = (unsigned short)(y1 / TILE);
+                const int wx = tr.y - tr.x + 1;
+                nt = wx * (tr.w - tr.z + 1);
+                if (nt <= 4) {  // claim the slots now; k_emit needs no atomics for this sphere
+#pragma unroll
+                    for (int j = 0; j < 4; ++j)
+                        if (j < nt) sl[j] = atomicAdd(&a.tile_count[(tr.z + j / wx) * cam.ntx + tr.x + j % wx], 1);
+                } else {
+                    for (int ty = tr.z; ty <= tr.w; ++ty)
+                        for (int tx = tr.x; tx <= tr.y; ++tx) atomicAdd(&a.tile_count_big[ty * cam.ntx + tx], 1);
+                }
+            }
+            a.trect[i] = tr;
+        }
+
+        // exact quantities (bit-identical formulas to the reference): earliest depth and projected radius
+        double e, pr;
+        if (pin) {
+            const double d2 = cx * cx + cy * cy + cz * cz;
             e = sqrt(d2) - r;
             pr = (cam.focal * r / sqrt(fmax(d2 - r * r, 1e-300))) * cam.ppu;
             if (d2 <= r * r) pr = (double)(w > h ? w : h);
         } else {
-            lo_x = cx - r; hi_x = cx + r; lo_y = cy - r; hi_y = cy + r;
-            u_c = w / 2.0 + cx * cam.ppu;
-            v_c = h / 2.0 + cy * cam.ppu;
             e = cz - r;
             pr = r * cam.ppu;
         }
         a.proj_r[i] = pr;
         if (a.proj_r_out) a.proj_r_out[i] = pr;
         if (!a.records_only) {
+            if (!on) e = INFINITY;
+            if (a.earliest) a.earliest[i] = e;
+            a.key[i] = order_key(e);
             // Screen-space filter record for k_raster: a pixel can only hit the sphere if it lies in
             // the circle around the projected centre with radius f (tan(theta + alpha) - tan(theta))
             // (theta: centre off the optical axis, alpha = asin(r/|c|)), which bounds the projected
             // outline.  Padded for the float32 evaluation; infinite (always passes) when the sphere
             // reaches the camera plane or contains the camera.
             double pcx = 0.0, pcy = 0.0, rho = INFINITY;
-            if (cam.mode == SS_MODE_PINHOLE) {
+            if (pin) {
                 const double n2 = cx * cx + cy * cy + cz * cz, rr = r * r;
                 if (cz > r && n2 > rr) {
-                    const double tan_t = sqrt(cx * cx + cy * cy) / cz;
-                    const double tan_a = r / sqrt(n2 - rr);
+                    const double tan_t = sqrt(cx * cx + cy * cy) * inv_cz;
+                    const double tan_a = pr * cam.inv_f_ppu;  // r / sqrt(|c|^2 - r^2), already computed
                     const double den = 1.0 - tan_t * tan_a;
                     if (den > 1e-6) {
                         rho = cam.focal * ((tan_t + tan_a) / den - tan_t);
-                        pcx = cam.focal * cx / cz;
-                        pcy = cam.focal * cy / cz;
+                        pcx = cam.focal * cx * inv_cz;
+                        pcy = cam.focal * cy * inv_cz;
                     }
                 }
             } else {
@@ -168,38 +213,7 @@ __global__ void __launch_bounds__(256) k_project(ProjectArgs a) {
             }
             const float rho_pad = (float)(rho * (1.0 + 1e-5) + 4e-7 * (fabs(pcx) + fabs(pcy) + cam.sensor_w));
             a.flt[i] = make_float4((float)pcx, (float)pcy, rho_pad * rho_pad * 1.000001f, 0.0f);
-        }
-        if (!a.records_only) {
-            int x0, x1, y0, y1; bool out_x, out_y;
-            discretize_extent(w / 2.0 + lo_x * cam.ppu, w / 2.0 + hi_x * cam.ppu, u_c, w, x0, x1, out_x);
-            discretize_extent(h / 2.0 + lo_y * cam.ppu, h / 2.0 + hi_y * cam.ppu, v_c, h, y0, y1, out_y);
-            on = !(behind || empty_x || empty_y || out_x || out_y) && !bad;
-            if (!on) e = INFINITY;
-            if (a.rect) {
-                a.rect[4 * i] = x0; a.rect[4 * i + 1] = x1; a.rect[4 * i + 2] = y0; a.rect[4 * i + 3] = y1;
-            }
-            if (a.on_sensor) a.on_sensor[i] = on ? 1 : 0;
-            if (a.earliest) a.earliest[i] = e;
-            a.key[i] = order_key(e);
-            ushort4 tr;
-            if (on) {
-                tr.x = (unsigned short)(x0 / TILE); tr.y = (unsigned short)(x1 / TILE);
-                tr.z = (unsigned short)(y0 / TILE); tr.w = (unsigned short)(y1 / TILE);
-                const int wx = tr.y - tr.x + 1, nt = wx * (tr.w - tr.z + 1);
-                if (nt <= 4) {  // claim the slots now; k_emit needs no atomics for this sphere
-                    int sl[4] = {0, 0, 0, 0};
-#pragma unroll
-                    for (int j = 0; j < 4; ++j)
-                        if (j < nt) sl[j] = atomicAdd(&a.tile_count[(tr.z + j / wx) * cam.ntx + tr.x + j % wx], 1);
-                    a.slot4[i] = make_int4(sl[0], sl[1], sl[2], sl[3]);
-                } else {
-                    for (int ty = tr.z; ty <= tr.w; ++ty)
-                        for (int tx = tr.x; tx <= tr.y; ++tx) atomicAdd(&a.tile_count_big[ty * cam.ntx + tx], 1);
-                }
-            } else {
-                tr.x = 1; tr.y = 0; tr.z = 1; tr.w = 0;
-            }
-            a.trect[i] = tr;
+            if (on && nt <= 4) a.slot4[i] = make_int4(sl[0], sl[1], sl[2], sl[3]);
         }
     }
     if (!a.records_only) {

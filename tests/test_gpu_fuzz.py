@@ -1,0 +1,86 @@
+"""GPU: randomised geometry against the oracle -- wide and narrow fields of view, rotated cameras,
+spheres in front of / around / behind / containing the camera, sub-pixel to screen-filling radii,
+ragged image sizes.  Exercises the conservative float32 filter, the per-warp culling masks and the
+trig fall-back of the extents; ids, tile lists and counters must stay exact."""
+import numpy as np
+import pytest
+
+from helpers import FWD_ATOL, FWD_RTOL, assert_close, grad_close
+
+pytestmark = pytest.mark.gpu
+
+
+def _random_case(seed):
+    rng = np.random.default_rng(seed)
+    mode = "orthographic" if seed % 4 == 3 else "pinhole"
+    w, h = int(rng.integers(17, 90)), int(rng.integers(17, 90))
+    focal = float(rng.uniform(0.8, 6.0))
+    sensor = float(rng.uniform(1.0, 4.0)) if mode == "pinhole" else float(rng.uniform(6.0, 20.0))
+    m = int(rng.integers(5, 120))
+    d = int(rng.choice([1, 2, 3, 4, 6]))
+    k = int(rng.choice([1, 3, 5, 8, 11]))
+    if seed % 3 == 0:   # cloud in front of the camera
+        pos = np.column_stack([rng.uniform(-4, 4, m), rng.uniform(-4, 4, m), rng.uniform(2, 40, m)])
+        rad = rng.uniform(0.01, 2.5, m)
+    elif seed % 3 == 1:  # cloud all around the camera, some spheres contain it
+        pos = rng.uniform(-6, 6, (m, 3))
+        rad = rng.uniform(0.05, 4.0, m)
+    else:                # mixture of tiny far spheres and huge near ones
+        pos = np.column_stack([rng.uniform(-8, 8, m), rng.uniform(-8, 8, m), rng.uniform(-2, 44, m)])
+        rad = np.where(rng.uniform(size=m) < 0.2, rng.uniform(3, 12, m), rng.uniform(1e-3, 0.3, m))
+    opa = rng.uniform(-0.2, 1.3, m)
+    feat = rng.uniform(0, 1, (m, d))
+    bg = rng.uniform(0, 1, d)
+    t = rng.uniform(-0.5, 0.5, 3)
+    if seed % 2 == 0:
+        vec = np.concatenate([t, rng.uniform(-0.4, 0.4, 3), [focal, sensor]])
+    else:
+        a6 = np.array([1, 0, 0, 0, 1, 0], float) + rng.uniform(-0.3, 0.3, 6)
+        vec = np.concatenate([t, a6, [focal, sensor]])
+    f32 = np.float32
+    return dict(pos=pos.astype(f32), rad=rad.astype(f32), opa=opa.astype(f32), feat=feat.astype(f32),
+                bg=bg.astype(f32), vec=vec, w=w, h=h, mode=mode, k=k, gamma=float(rng.uniform(0.03, 0.6)),
+                tau=0.0 if seed % 5 else 0.02, near=0.1, far=float(rng.uniform(20, 60)), rng=rng)
+
+
+@pytest.mark.parametrize("seed", range(40))
+def test_random_geometry_vs_oracle(engine, seed):
+    from oracle import oracle as orc
+    from paper_2004_07484_b200 import CameraSpec, camera_from_vector
+    c = _random_case(seed)
+    cam = camera_from_vector(c["vec"], c["w"], c["h"], near=c["near"], far=c["far"], mode=c["mode"])
+    ocam = orc.camera_from_vector(c["vec"], c["w"], c["h"], near=c["near"], far=c["far"], mode=c["mode"])
+    spec = CameraSpec.from_camera(cam)
+    args = (c["pos"], c["rad"], c["opa"], c["feat"], c["bg"])
+    ref = orc.render_forward(*args, ocam, gamma=c["gamma"], tau=c["tau"], top_k=c["k"])
+    f = engine.forward(*args, spec, gamma=c["gamma"], tau=c["tau"], top_k=c["k"], collect_stats=True, debug=True)
+    b = orc.compute_bounds(c["pos"], c["rad"], ocam)
+    rect = f["rect"].cpu().numpy()
+    on = f["on_sensor"].cpu().numpy().astype(bool)
+    assert np.array_equal(on, b["on_sensor"])
+    for j, name in enumerate(("x_min", "x_max", "y_min", "y_max")):
+        assert np.array_equal(rect[:, j], b[name]), name
+    starts, ids = engine.tile_lists(len(c["rad"]), c["feat"].shape[1], c["w"], c["h"], c["k"])
+    o_ids, o_starts = orc.tile_lists(c["pos"], c["rad"], ocam)
+    assert np.array_equal(starts, o_starts) and np.array_equal(ids, o_ids)
+    st = f["status"]
+    assert st["hits_blended"] == ref["stats"]["hits_blended"]
+    if c["tau"] == 0.0:
+        assert st["candidates_tested"] == ref["stats"]["candidates_tested"]
+        assert np.array_equal(f["ids"].permute(1, 2, 0).cpu().numpy(), ref["ids"])
+    assert_close(f["image"].cpu().numpy(), ref["image"], 2 * FWD_RTOL, 2 * FWD_ATOL, "image")
+    if c["tau"] == 0.0:
+        up = c["rng"].normal(size=ref["image"].shape).astype(np.float32)
+        out = engine.backward(*args, spec, f, up, gamma=c["gamma"], eps=1e-2, normalize=bool(seed % 2),
+                              gate=bool(seed % 2))
+        gr = orc.render_backward(*args, ocam, ref, up.astype(np.float64), normalize=bool(seed % 2),
+                                 gate=bool(seed % 2))
+        assert np.array_equal(out["pixel_count"].cpu().numpy(), gr["pixel_count"])
+        grad_close(out["d_pos"].cpu().numpy(), gr["d_position"], "d_position", rtol=2e-4)
+        grad_close(out["d_rad"].cpu().numpy(), gr["d_radius"], "d_radius", rtol=2e-4)
+        grad_close(out["d_opa"].cpu().numpy(), gr["d_opacity"], "d_opacity", rtol=2e-4)
+        grad_close(out["d_feat"].cpu().numpy(), gr["d_feature"], "d_feature", rtol=2e-4)
+        cg = out["cam_grad"].cpu().numpy()
+        grad_close(cg[0:3], gr["d_translation"], "d_translation", rtol=2e-4)
+        grad_close(cg[3:12].reshape(3, 3), gr["grad_rot_matrix"], "dL/dR", rtol=2e-4)
+        grad_close(cg[12:14], [gr["d_focal"], gr["d_sensor_width"]], "intrinsics", rtol=2e-4)

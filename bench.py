@@ -99,6 +99,14 @@ def algorithmic_bytes(T, S, U, M=COUNT, P=SIZE * SIZE, d=D, K=TOP_K):
     return fwd, bwd, raster
 
 
+def host_threads():
+    """Host cores this process may use (torchrun exports OMP_NUM_THREADS=1, so do not ask OpenMP)."""
+    try:
+        return max(1, len(os.sched_getaffinity(0)))
+    except AttributeError:
+        return max(1, os.cpu_count() or 1)
+
+
 def cpu_frame_seconds(threads, repeats=1):
     """One full C3 frame (fwd + bwd) on the CPU oracle port of the reference; returns seconds/frame."""
     from oracle import oracle as orc
@@ -122,7 +130,7 @@ def run_reference(args, rank):
         return
     from oracle import oracle as orc
     orc.build()
-    threads = orc.num_threads_available()
+    threads = host_threads()
     warm = cpu_frame_seconds(threads) if args.warmup > 0 else []
     # bounded sample: full frames, as many of the K requested as fit in ~2 minutes of CPU time
     first = cpu_frame_seconds(threads, repeats=1)
@@ -170,10 +178,17 @@ def main():
     from paper_2004_07484_b200.synthetic import benchmark_scene, orbit_camera_vectors
 
     assert torch.cuda.is_available(), "bench.py needs a CUDA device (no CPU fallback)"
-    torch.cuda.set_device(local_rank)
-    device = torch.device("cuda", local_rank)
+    # One GPU per rank.  SS_DIST_BACKEND=gloo lets several ranks share a GPU to smoke-test the N > 1 code
+    # path on a single-GPU box (NCCL refuses duplicate devices); the real run uses NCCL over NVLink.
+    backend = os.environ.get("SS_DIST_BACKEND", "nccl")
+    dev_index = local_rank % torch.cuda.device_count()
+    torch.cuda.set_device(dev_index)
+    device = torch.device("cuda", dev_index)
     if world > 1:
-        dist.init_process_group("nccl", device_id=device)
+        if backend == "nccl":
+            dist.init_process_group("nccl", device_id=device)
+        else:
+            dist.init_process_group(backend)
     vpr = args.views_per_rank or (1 if world == 1 else 8)
     n_views = vpr * world
 
@@ -209,7 +224,7 @@ def main():
     torch.cuda.synchronize()
     if world > 1:
         dist.barrier()
-    sampler = ClockSampler(local_rank)
+    sampler = ClockSampler(dev_index)
     sampler.start()
     ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
     launches0 = _lib.launch_count()
@@ -291,7 +306,7 @@ def main():
                        "cache": "L2 flushed between timed steps (256 MB write, outside the timed region)",
                        "pairs_T": T, "filled_slots_S": filled, "touched_spheres_U": touched,
                        "collective": ("none" if world == 1 else
-                                      f"1 NCCL sum-allreduce of {grads.allreduce_bytes()} B per step")},
+                                      f"1 {backend} sum-allreduce of {grads.allreduce_bytes()} B per step")},
             "clocks": clocks,
             "e2e": {"value": e2e_value, "unit": "frames/s", "h2d_bytes_per_step": h2d_b, "d2h_bytes_per_step": d2h_b,
                     "steps": e2e_steps,
@@ -315,7 +330,7 @@ def main():
         if world == 1 and not args.no_cpu_baseline:
             from oracle import oracle as orc
             orc.build()
-            threads = orc.num_threads_available()
+            threads = host_threads()
             secs = cpu_frame_seconds(threads, repeats=1)[0]
             line["cpu_baseline"] = {"value": 1.0 / secs, "unit": "frames/s", "cores": threads, "kind": "port",
                                     "sample": "1 full C3 frame (fwd+bwd, tau=0.01) on the float64 oracle port, "

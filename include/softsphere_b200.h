@@ -198,6 +198,45 @@ int ss_read_status(const void *workspace, SsStatus *out_host, void *stream);
 int ss_debug_tile_lists(const SsDims *dims, const void *workspace, int32_t *tile_starts_out,
                         int32_t *ids_out, void *stream);
 
+/* ------------------------------------------------------------------------------------------------
+ * the step either side of the render path in the reference's fit loop.
+ *
+ *   ss_photometric_loss <- photometric_loss           optim.py:87-97
+ *   ss_fit_step         <- opacity_depth_regularizer  optim.py:100-121  (gradients added in place)
+ *                          visibility += pixel_count  optim.py:307
+ *                          adam_step x 4 groups + radius floor  optim.py:142-154, :309-329
+ *   ss_adam_flat        <- adam_step on one array     optim.py:142-154  (camera vectors)
+ * ---------------------------------------------------------------------------------------------- */
+
+/* loss_out (device, float64) = mean |image - target|; upstream = sign(image - target) / n (0 at ties). */
+int ss_photometric_loss(const float *image, const float *target, float *upstream, int64_t n,
+                        double *loss_out, void *stream);
+
+/* Parameter groups: 0 position, 1 radius, 2 opacity, 3 feature.  lr[g] == 0 freezes group g
+ * (its state pointers may be NULL); step[g] is the group's Adam step count AFTER this update (>= 1). */
+typedef struct SsFitStepArgs {
+    int64_t num_spheres;
+    int32_t feature_dim;
+    int32_t pad_;
+    float *pos, *rad, *opa, *feat;                       /* parameters, updated in place */
+    const float *d_pos, *d_rad, *d_opa, *d_feat;         /* gradients from ss_backward */
+    const int32_t *pixel_count;                          /* from ss_backward (may be NULL without visibility) */
+    int32_t *visibility;                                 /* += pixel_count, or NULL */
+    float *m_pos, *v_pos, *m_rad, *v_rad, *m_opa, *v_opa, *m_feat, *v_feat; /* Adam moments, in place */
+    double lr[4];
+    int64_t step[4];
+    double beta1, beta2, adam_eps;
+    double radius_min;                                   /* radius floor (FitConfig.radius_min) */
+    double lambda_od;                                    /* opacity-depth regulariser weight; 0 disables */
+    SsCamera cam;                                        /* for the regulariser */
+    double *energy;                                      /* device float64: regulariser energy, or NULL */
+} SsFitStepArgs;
+
+int ss_fit_step(const SsFitStepArgs *args, void *stream);
+
+int ss_adam_flat(float *params, const float *grads, float *m, float *v, int64_t n, double lr, double beta1,
+                 double beta2, double adam_eps, int64_t step, int use_floor, double floor_value, void *stream);
+
 /* Number of kernels this library has launched in this process (bench.py's gpu_launches). */
 int64_t ss_launch_count(void);
 

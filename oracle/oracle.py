@@ -12,7 +12,8 @@ the small host-side pieces of the reference in NumPy:
   :79-97, :216-249;
 * rotation-parameter VJPs                   -- softsphere/camera.py:57-76, :100-117;
 * blend-parameter clamping / validation     -- softsphere/blend.py:38-45;
-* scene validation                          -- softsphere/scene.py:91-114.
+* scene validation                          -- softsphere/scene.py:91-114;
+* the fit-loop step      -- softsphere/optim.py:87-154, :286-329.
 
 Parity is pinned: oracle/pin_against_reference.py checks every entry point
 against the imported reference and writes tests/golden/*.npz.
@@ -108,17 +109,6 @@ def rotation_from_6d(a):
         raise OracleConfigurationError("6d rotation: columns are near-parallel")
     c2 = w / nw
     return np.stack([c1, c2, np.cross(c1, c2)], axis=1)
-
-
-def _numeric_vjp(fn, x, g, h=1e-6):
-    x = np.asarray(x, dtype=np.float64).copy()
-    out = np.zeros_like(x)
-    for i in range(x.size):
-        xp, xm = x.copy(), x.copy()
-        xp[i] += h
-        xm[i] -= h
-        out[i] = np.sum(g * (fn(xp) - fn(xm))) / (2 * h)
-    return out
 
 
 def axis_angle_vjp(v, grad_matrix):
@@ -435,3 +425,68 @@ def benchmark_scene(count, width, height, seed=0, d=3, profile="uniform", aspect
     bg = np.zeros(d, np.float32)
     cam_vec = np.array([0, 0, 0, 0, 0, 0, f, s], dtype=np.float64)
     return pos, rad, opa, feat, bg, cam_vec
+
+
+# --------------------------------------------------------------------------- fit-loop step
+# NumPy restatements of softsphere/optim.py:87-97 (photometric_loss), :100-121
+# (opacity_depth_regularizer) and :142-154 (adam_step); pinned by pin_against_reference.py.
+
+def photometric_loss(rendered, target):
+    """(mean |rendered - target|, sign(diff) / n)."""
+    diff = np.asarray(rendered, dtype=np.float64) - np.asarray(target, dtype=np.float64)
+    n = diff.size
+    return float(np.abs(diff).sum() / n), np.sign(diff) / n
+
+
+def opacity_depth_regularizer(pos, opa, cam: OracleCamera, lambda_od):
+    """Energy sum(-lambda z_i o_i) and its gradients w.r.t. position and (unclamped) opacity."""
+    pos = _f64(pos, (-1, 3))
+    opa = _f64(opa, (-1,))
+    m = pos.shape[0]
+    if lambda_od == 0.0 or m == 0:
+        return 0.0, np.zeros((m, 3)), np.zeros(m)
+    zeta = ((pos - cam.translation) @ cam.rotation.T)[:, 2]
+    span = cam.far - cam.near
+    z = (cam.far - np.clip(zeta, cam.near, cam.far)) / span
+    o = np.clip(opa, 0.0, 1.0)
+    inside = (zeta > cam.near) & (zeta < cam.far)
+    dzeta = np.where(inside, lambda_od * o / span, 0.0)
+    return float(lambda_od * np.sum(-z * o)), dzeta[:, None] * cam.rotation[2][None, :], -lambda_od * z
+
+
+def adam_step(params, grads, m, v, t, lr, beta1=0.9, beta2=0.999, adam_eps=1e-8):
+    """One bias-corrected Adam update; returns (params', m', v', t + 1)."""
+    params, grads = np.asarray(params, np.float64), np.asarray(grads, np.float64)
+    t = t + 1
+    m = beta1 * m + (1 - beta1) * grads
+    v = beta2 * v + (1 - beta2) * grads * grads
+    m_hat = m / (1 - beta1 ** t)
+    v_hat = v / (1 - beta2 ** t)
+    return params - lr * m_hat / (np.sqrt(v_hat) + adam_eps), m, v, t
+
+
+def fit_step(scene, cam: OracleCamera, target, state, cfg, threads=1):
+    """One iteration of the reference's fit loop body (optim.py:286-329) for one observation.
+    scene = dict(pos, rad, opa, feat, bg) of float64 arrays (updated copies are returned);
+    state = dict(group -> (m, v, t)) for groups pos/rad/opa/feat; cfg = dict with lr_* , beta1, beta2,
+    adam_eps, gamma, epsilon, tau, top_k, lambda_od, radius_min, normalize_grads, gate.
+    Returns (loss, scene', state', grads)."""
+    f = render_forward(scene["pos"], scene["rad"], scene["opa"], scene["feat"], scene["bg"], cam,
+                       gamma=cfg["gamma"], eps=cfg["epsilon"], tau=cfg["tau"], top_k=cfg["top_k"], threads=threads)
+    loss, upstream = photometric_loss(f["image"], target)
+    e, r_dpos, r_dopa = opacity_depth_regularizer(scene["pos"], scene["opa"], cam, cfg["lambda_od"])
+    loss += e
+    g = render_backward(scene["pos"], scene["rad"], scene["opa"], scene["feat"], scene["bg"], cam, f, upstream,
+                        normalize=cfg["normalize_grads"], gate=cfg["gate"], threads=threads)
+    g["d_position"] = g["d_position"] + r_dpos
+    g["d_opacity"] = g["d_opacity"] + r_dopa
+    new_scene, new_state = dict(scene), dict(state)
+    for key, gname, lr in (("pos", "d_position", cfg["lr_position"]), ("rad", "d_radius", cfg["lr_radius"]),
+                           ("opa", "d_opacity", cfg["lr_opacity"]), ("feat", "d_feature", cfg["lr_feature"])):
+        if lr > 0:
+            m, v, t = state[key]
+            p, m, v, t = adam_step(scene[key], g[gname], m, v, t, lr, cfg["beta1"], cfg["beta2"], cfg["adam_eps"])
+            if key == "rad":
+                p = np.maximum(p, cfg["radius_min"])
+            new_scene[key], new_state[key] = p, (m, v, t)
+    return loss, new_scene, new_state, g

@@ -238,6 +238,80 @@ def pin_known_answers():
     assert np.abs(img - f["image"][4, 4]).max() < 1e-12
 
 
+def pin_fit_step(write=True):
+    """photometric_loss, opacity_depth_regularizer, adam_step and three iterations
+    of the fit loop body (optim.py:286-329) -- reference vs oracle, then golden vectors."""
+    from softsphere import optim as ro
+    rng = np.random.default_rng(2024)
+    a, b = rng.uniform(0, 1, (9, 7, 3)), rng.uniform(0, 1, (9, 7, 3))
+    b[0, 0] = a[0, 0]  # ties -> sign 0
+    l_ref, u_ref = ro.photometric_loss(a, b)
+    l_or, u_or = orc.photometric_loss(a, b)
+    assert l_ref == l_or and np.array_equal(u_ref, u_or)
+    sc = random_scene(rng, 30, depth=(0.05, 50.0))
+    vec = np.array([0.3, -0.2, 0.5, 0.02, -0.03, 0.01, 5.0, 2.0])
+    case = dict(scene=sc, vec=vec, w=40, h=32, mode="pinhole", near=0.1, far=45.0, gamma=0.2, eps=1e-2, tau=0.0,
+                top_k=5)
+    scene, cam, _ = ref_objects(case)
+    ocam = orc.camera_from_vector(vec, 40, 32)
+    e_ref, dp_ref, do_ref = ro.opacity_depth_regularizer(scene, cam, 0.37)
+    e_or, dp_or, do_or = orc.opacity_depth_regularizer(sc[0], sc[2], ocam, 0.37)
+    close(e_ref, e_or, "od energy", 1e-14)
+    close(dp_ref, dp_or, "od d_position", 1e-14)
+    close(do_ref, do_or, "od d_opacity", 1e-14)
+    cfg = ro.FitConfig(lr_position=2e-3, lr_radius=1e-3, lr_opacity=1e-2, lr_feature=2e-2, lambda_od=0.05)
+    st = ro.AdamState.like(sc[0].astype(np.float64))
+    p_ref = sc[0].astype(np.float64)
+    p_or, m_or, v_or, t_or = p_ref.copy(), np.zeros_like(p_ref), np.zeros_like(p_ref), 0
+    for _ in range(3):
+        g = rng.normal(size=p_ref.shape)
+        p_ref = ro.adam_step(p_ref, g, st, 2e-3, cfg)
+        p_or, m_or, v_or, t_or = orc.adam_step(p_or, g, m_or, v_or, t_or, 2e-3)
+    close(p_ref, p_or, "adam params", 1e-15)
+    close(st.v, v_or, "adam v", 1e-15)
+
+    # three iterations of the loop body on one observation (normalised, gated gradients)
+    target = rng.uniform(0, 1, (32, 40, 3))
+    params = ss.BlendParams(gamma=0.2, epsilon=1e-2, tau=0.0, top_k=5)
+    r_scene = scene.copy()
+    states = {k: ro.AdamState.like(getattr(r_scene, n)) for k, n in
+              (("pos", "positions"), ("rad", "radii"), ("opa", "opacities"), ("feat", "features"))}
+    o_scene = dict(pos=sc[0].astype(np.float64), rad=sc[1].astype(np.float64), opa=sc[2].astype(np.float64),
+                   feat=sc[3].astype(np.float64), bg=sc[4].astype(np.float64))
+    o_state = {k: (np.zeros_like(o_scene[k]), np.zeros_like(o_scene[k]), 0) for k in ("pos", "rad", "opa", "feat")}
+    o_cfg = dict(lr_position=2e-3, lr_radius=1e-3, lr_opacity=1e-2, lr_feature=2e-2, beta1=0.9, beta2=0.999,
+                 adam_eps=1e-8, gamma=0.2, epsilon=1e-2, tau=0.0, top_k=5, lambda_od=0.05, radius_min=1e-6,
+                 normalize_grads=True, gate=True)
+    losses = []
+    for _ in range(3):
+        img, buf, _ = ss.render_forward(r_scene, cam, params)
+        loss, up = ro.photometric_loss(img.data, target)
+        e, rdp, rdo = ro.opacity_depth_regularizer(r_scene, cam, cfg.lambda_od)
+        loss += e
+        g, _cg = ss.render_backward(r_scene, cam, params, buf, up)
+        g.d_position += rdp
+        g.d_opacity += rdo
+        r_scene.positions = ro.adam_step(r_scene.positions, g.d_position, states["pos"], cfg.lr_position, cfg)
+        r_scene.radii = np.maximum(ro.adam_step(r_scene.radii, g.d_radius, states["rad"], cfg.lr_radius, cfg),
+                                   cfg.radius_min)
+        r_scene.opacities = ro.adam_step(r_scene.opacities, g.d_opacity, states["opa"], cfg.lr_opacity, cfg)
+        r_scene.features = ro.adam_step(r_scene.features, g.d_feature, states["feat"], cfg.lr_feature, cfg)
+        o_loss, o_scene, o_state, _ = orc.fit_step(o_scene, ocam, target, o_state, o_cfg)
+        close(loss, o_loss, "fit loss", 1e-9)
+        losses.append(loss)
+    close(r_scene.positions, o_scene["pos"], "fit positions", 1e-9)
+    close(r_scene.radii, o_scene["rad"], "fit radii", 1e-9)
+    close(r_scene.opacities, o_scene["opa"], "fit opacities", 1e-8, 1e-12)
+    close(r_scene.features, o_scene["feat"], "fit features", 1e-8, 1e-12)
+    if write:
+        np.savez_compressed(os.path.join(GOLDEN, "fit_step.npz"), pos=sc[0], rad=sc[1], opa=sc[2], feat=sc[3],
+                            bg=sc[4], cam_vec=vec, width=40, height=32, target=target.astype(np.float32),
+                            losses=np.array(losses), pos_out=r_scene.positions, rad_out=r_scene.radii,
+                            opa_out=r_scene.opacities, feat_out=r_scene.features,
+                            pm_a=a.astype(np.float32), pm_b=b.astype(np.float32))
+    print("fit step (photometric loss, regulariser, adam, 3 loop iterations): ok")
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--no-write", action="store_true")
@@ -249,6 +323,7 @@ def main():
         st = run_case(case, write=not args.no_write)
         print(f"{case['name']:28s} ok  (tested={st.candidates_tested} hits={st.hits_blended} "
               f"stopped={st.pixels_early_stopped})")
+    pin_fit_step(write=not args.no_write)
     print("oracle pinned against reference; golden fixtures in", GOLDEN)
 
 

@@ -11,5 +11,6 @@ from .types import (AXIS_ANGLE, ORTHOGRAPHIC, PINHOLE, SIX_D, BackwardBuffer, Bl
 from .api import SoftsphereAdapter, render_backward, render_forward
 from .engine import CameraSpec, RenderEngine, default_engine
 from .function import Renderer, SphereRender
+from .optim import AdamState, DeviceFit, FitConfig, adam_step, photometric_loss, photometric_loss_device
 
 __version__ = "0.1.0"

@@ -67,6 +67,18 @@ class SsBackwardArgs(C.Structure):
                 ("cam_grad", _P)]
 
 
+class SsFitStepArgs(C.Structure):
+    _fields_ = [("num_spheres", C.c_int64), ("feature_dim", C.c_int32), ("pad_", C.c_int32),
+                ("pos", _P), ("rad", _P), ("opa", _P), ("feat", _P),
+                ("d_pos", _P), ("d_rad", _P), ("d_opa", _P), ("d_feat", _P),
+                ("pixel_count", _P), ("visibility", _P),
+                ("m_pos", _P), ("v_pos", _P), ("m_rad", _P), ("v_rad", _P), ("m_opa", _P), ("v_opa", _P),
+                ("m_feat", _P), ("v_feat", _P),
+                ("lr", C.c_double * 4), ("step", C.c_int64 * 4),
+                ("beta1", C.c_double), ("beta2", C.c_double), ("adam_eps", C.c_double),
+                ("radius_min", C.c_double), ("lambda_od", C.c_double), ("cam", SsCamera), ("energy", _P)]
+
+
 class SsStatus(C.Structure):
     _fields_ = [("flags", C.c_int64), ("spheres_on_sensor", C.c_int64), ("num_pairs", C.c_int64),
                 ("candidates_tested", C.c_int64), ("hits_blended", C.c_int64),
@@ -75,7 +87,7 @@ class SsStatus(C.Structure):
 
 
 EXPORTS = ("ss_abi_version", "ss_status_string", "ss_last_cuda_error", "ss_workspace_bytes", "ss_workspace_init",
-           "ss_forward", "ss_backward", "ss_read_status", "ss_debug_tile_lists", "ss_launch_count",
+           "ss_forward", "ss_backward", "ss_read_status", "ss_photometric_loss", "ss_fit_step", "ss_adam_flat", "ss_debug_tile_lists", "ss_launch_count",
            "ss_profile_enable", "ss_profile_enable_mask", "ss_profile_collect", "ss_profile_kernel_count", "ss_profile_kernel_name")
 
 _lib = None
@@ -106,6 +118,13 @@ def load():
     lib.ss_forward.argtypes = [C.POINTER(SsForwardArgs), C.c_void_p]
     lib.ss_backward.restype = C.c_int
     lib.ss_backward.argtypes = [C.POINTER(SsBackwardArgs), C.c_void_p]
+    lib.ss_photometric_loss.restype = C.c_int
+    lib.ss_photometric_loss.argtypes = [C.c_void_p, C.c_void_p, C.c_void_p, C.c_int64, C.c_void_p, C.c_void_p]
+    lib.ss_fit_step.restype = C.c_int
+    lib.ss_fit_step.argtypes = [C.POINTER(SsFitStepArgs), C.c_void_p]
+    lib.ss_adam_flat.restype = C.c_int
+    lib.ss_adam_flat.argtypes = [C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p, C.c_int64, C.c_double, C.c_double,
+                                 C.c_double, C.c_double, C.c_int64, C.c_int, C.c_double, C.c_void_p]
     lib.ss_read_status.restype = C.c_int
     lib.ss_read_status.argtypes = [C.c_void_p, C.POINTER(SsStatus), C.c_void_p]
     lib.ss_debug_tile_lists.restype = C.c_int

@@ -1,0 +1,183 @@
+"""the step either side of the render path in the reference's fit loop
+(softsphere/optim.py), on the device.
+
+  photometric_loss(rendered, target)        optim.py:87-97   (reference signature, NumPy in/out)
+  adam_step(params, grads, state, lr, cfg)  optim.py:142-154 (reference signature, NumPy in/out)
+  DeviceFit                                 the body of fit's loop (optim.py:280-329) for one observation:
+                                            forward -> L1 loss + upstream -> backward -> regulariser +
+                                            visibility + per-group Adam with radius floor, all device resident
+
+Everything runs in the sm_100a kernels of csrc/ss_optim.cu (k_photometric, k_fit_step, k_adam_flat)
+through the C ABI; there is no CPU fallback.  Pruning, subdivision, checkpoints and the epoch
+shuffling of `fit` stay out of scope.
+"""
+from __future__ import annotations
+
+import ctypes as C
+from dataclasses import dataclass, field
+
+import numpy as np
+import torch
+
+from . import _lib
+from .engine import CameraSpec, RenderEngine, _ptr, _raise_for, default_engine
+from .types import ConfigurationError, DivergenceError, ValidationError
+
+RADIUS_MIN = 1e-6
+
+
+@dataclass
+class FitConfig:
+    """The fields of the reference's FitConfig that the per-step update uses (optim.py:33-70)."""
+    lr_position: float = 1e-3
+    lr_radius: float = 1e-3
+    lr_opacity: float = 1e-2
+    lr_feature: float = 1e-2
+    lr_camera: float = 0.0
+    beta1: float = 0.9
+    beta2: float = 0.999
+    adam_eps: float = 1e-8
+    gamma: float = 0.1
+    epsilon: float = 1e-2
+    tau: float = 0.01
+    top_k: int = 5
+    lambda_od: float = 0.0
+    radius_min: float = RADIUS_MIN
+    normalize_grads: bool = True
+    gate: bool = True
+
+    def __post_init__(self):
+        for name in ("lr_position", "lr_radius", "lr_opacity", "lr_feature", "lr_camera"):
+            if getattr(self, name) < 0:
+                raise ConfigurationError(f"{name} must be >= 0")
+
+
+@dataclass
+class AdamState:
+    m: np.ndarray
+    v: np.ndarray
+    t: int = 0
+
+    @staticmethod
+    def like(x) -> "AdamState":
+        return AdamState(m=np.zeros_like(x, dtype=np.float64), v=np.zeros_like(x, dtype=np.float64))
+
+
+def _stream(dev):
+    return C.c_void_p(torch.cuda.current_stream(dev).cuda_stream)
+
+
+def photometric_loss_device(image: torch.Tensor, target: torch.Tensor):
+    """Device tensors in, (loss tensor float64[1], upstream tensor) out; one kernel, no sync."""
+    if image.shape != target.shape:
+        raise ValidationError(f"rendered shape {tuple(image.shape)} != target {tuple(target.shape)}")
+    lib = _lib.load()
+    image, target = image.contiguous(), target.contiguous()
+    upstream = torch.empty_like(image)
+    loss = torch.empty(1, dtype=torch.float64, device=image.device)
+    rc = lib.ss_photometric_loss(_ptr(image), _ptr(target), _ptr(upstream), image.numel(), _ptr(loss),
+                                 _stream(image.device))
+    if rc != _lib.SS_OK:
+        _raise_for(rc)
+    return loss, upstream
+
+
+def photometric_loss(rendered, target, device="cuda"):
+    """Mean absolute error and its subgradient image sign(diff)/n (reference signature)."""
+    rendered = np.asarray(rendered, dtype=np.float64)
+    target = np.asarray(target, dtype=np.float64)
+    if rendered.shape != target.shape:
+        raise ValidationError(f"rendered shape {rendered.shape} != target {target.shape}")
+    dev = default_engine(device).device
+    a = torch.from_numpy(rendered.astype(np.float32)).to(dev)
+    b = torch.from_numpy(target.astype(np.float32)).to(dev)
+    loss, up = photometric_loss_device(a, b)
+    return float(loss.item()), up.cpu().numpy().astype(np.float64)
+
+
+def adam_step(params, grads, state: AdamState, lr: float, config, device="cuda"):
+    """Bias-corrected Adam on one array (reference signature); state is updated in place."""
+    params = np.asarray(params, dtype=np.float64)
+    grads = np.asarray(grads, dtype=np.float64)
+    if params.shape != grads.shape or state.m.shape != params.shape:
+        raise ValidationError("adam_step: parameter/gradient/state shape mismatch")
+    lib = _lib.load()
+    dev = default_engine(device).device
+    t = lambda x: torch.from_numpy(np.ascontiguousarray(x, dtype=np.float32)).to(dev)
+    p, g, m, v = t(params), t(grads), t(state.m), t(state.v)
+    state.t += 1
+    rc = lib.ss_adam_flat(_ptr(p), _ptr(g), _ptr(m), _ptr(v), p.numel(), float(lr), float(config.beta1),
+                          float(config.beta2), float(config.adam_eps), int(state.t), 0, 0.0, _stream(dev))
+    if rc != _lib.SS_OK:
+        _raise_for(rc)
+    state.m = m.cpu().numpy().astype(np.float64).reshape(params.shape)
+    state.v = v.cpu().numpy().astype(np.float64).reshape(params.shape)
+    return p.cpu().numpy().astype(np.float64).reshape(params.shape)
+
+
+class DeviceFit:
+    """Device-resident scene + Adam moments + visibility; `step` is one iteration of the reference's
+    fit loop body for one observation (optim.py:286-329), without leaving the GPU."""
+
+    def __init__(self, pos, rad, opa, feat, bg, config: FitConfig = None, engine: RenderEngine = None,
+                 device="cuda"):
+        self.cfg = config or FitConfig()
+        self.engine = engine or RenderEngine(device)
+        dev = self.engine.device
+        f32 = lambda x, shape: torch.as_tensor(np.ascontiguousarray(x, dtype=np.float32)).reshape(shape).to(dev).clone()
+        bg = np.asarray(bg, dtype=np.float32).reshape(-1)
+        self.d = int(bg.shape[0])
+        self.pos, self.rad = f32(pos, (-1, 3)), f32(rad, (-1,))
+        self.opa, self.feat, self.bg = f32(opa, (-1,)), f32(feat, (-1, self.d)), f32(bg, (-1,))
+        self.m = int(self.pos.shape[0])
+        z = lambda t: torch.zeros_like(t)
+        self.moments = {k: (z(t), z(t)) for k, t in (("pos", self.pos), ("rad", self.rad), ("opa", self.opa),
+                                                     ("feat", self.feat))}
+        self.steps = [0, 0, 0, 0]
+        self.visibility = torch.zeros(self.m, dtype=torch.int32, device=dev)
+        self.energy = torch.zeros(1, dtype=torch.float64, device=dev)
+        self.last = None
+
+    def apply_gradients(self, grads: dict, cam: CameraSpec):
+        """k_fit_step on the outputs of RenderEngine.backward."""
+        cfg, lib = self.cfg, _lib.load()
+        a = _lib.SsFitStepArgs()
+        a.num_spheres, a.feature_dim = self.m, self.d
+        a.pos, a.rad, a.opa, a.feat = _ptr(self.pos), _ptr(self.rad), _ptr(self.opa), _ptr(self.feat)
+        a.d_pos, a.d_rad = _ptr(grads["d_pos"]), _ptr(grads["d_rad"])
+        a.d_opa, a.d_feat = _ptr(grads["d_opa"]), _ptr(grads["d_feat"])
+        a.pixel_count, a.visibility = _ptr(grads["pixel_count"]), _ptr(self.visibility)
+        (a.m_pos, a.v_pos), (a.m_rad, a.v_rad) = map(_ptr, self.moments["pos"]), map(_ptr, self.moments["rad"])
+        (a.m_opa, a.v_opa), (a.m_feat, a.v_feat) = map(_ptr, self.moments["opa"]), map(_ptr, self.moments["feat"])
+        lrs = (cfg.lr_position, cfg.lr_radius, cfg.lr_opacity, cfg.lr_feature)
+        for g, lr in enumerate(lrs):
+            if lr > 0:
+                self.steps[g] += 1
+            a.lr[g] = float(lr)
+            a.step[g] = max(self.steps[g], 1)
+        a.beta1, a.beta2, a.adam_eps = float(cfg.beta1), float(cfg.beta2), float(cfg.adam_eps)
+        a.radius_min, a.lambda_od = float(cfg.radius_min), float(cfg.lambda_od)
+        a.cam = cam.to_c()
+        a.energy = _ptr(self.energy)
+        rc = lib.ss_fit_step(C.byref(a), _stream(self.engine.device))
+        if rc != _lib.SS_OK:
+            _raise_for(rc)
+
+    def step(self, target: torch.Tensor, cam: CameraSpec, gamma: float = None, check: bool = False):
+        """forward -> loss/upstream -> backward -> fused update.  Returns the loss (float64 tensor [1]:
+        photometric + regulariser energy of the scene BEFORE the update, like the reference's trace)."""
+        cfg = self.cfg
+        g = cfg.gamma if gamma is None else gamma
+        f = self.engine.forward(self.pos, self.rad, self.opa, self.feat, self.bg, cam, gamma=g, eps=cfg.epsilon,
+                                tau=cfg.tau, top_k=cfg.top_k, check=check)
+        loss, upstream = photometric_loss_device(f["image"], target)
+        grads = self.engine.backward(self.pos, self.rad, self.opa, self.feat, self.bg, cam, f, upstream, gamma=g,
+                                     eps=cfg.epsilon, normalize=cfg.normalize_grads, gate=cfg.gate,
+                                     camera_grads=cfg.lr_camera > 0)
+        self.apply_gradients(grads, cam)
+        self.last = {"image": f["image"], "grads": grads}
+        return loss + self.energy
+
+    def check_finite(self, loss: torch.Tensor):
+        if not bool(torch.isfinite(loss).all()):
+            raise DivergenceError("non-finite loss")

@@ -144,10 +144,6 @@ constexpr float kLn2 = 0.6931471805599453f;
 #ifndef SS_RASTER_MINB
 #define SS_RASTER_MINB (SS_TOPK_SHARED ? 4 : 3)  // resident CTAs per SM the register allocation targets (d <= 4, K <= 8)
 #endif
-#ifndef SS_DRAIN_MIN_ACTIVE
-#define SS_DRAIN_MIN_ACTIVE 12
-#endif
-constexpr int DRAIN_MIN_ACTIVE = SS_DRAIN_MIN_ACTIVE;
 
 template <int DP, int KT, int MODE>
 __global__ void __launch_bounds__(TILE_PX, (KT <= 8 && DP <= 4) ? SS_RASTER_MINB : 1) k_raster(RasterArgs a) {
@@ -186,8 +182,9 @@ __global__ void __launch_bounds__(TILE_PX, (KT <= 8 && DP <= 4) ? SS_RASTER_MINB
         ux = xs / vn; uy = ys / vn; uz = cam.focal / vn;
     }
     // float32 sensor coordinates for the screen-space filter; an out-of-image (or finished) pixel
-    // is moved far away so it never passes
-    constexpr float kFar = 1e30f;
+    // gets a NaN coordinate so it never passes (arithmetic NaNs are canonical 0x7fffffff: sign bit
+    // clear, also against an infinite rho^2, where a huge finite coordinate would still pass)
+    const float kFar = __int_as_float(0x7fffffff);
     float fx = valid ? (float)xs : kFar;
     float fy = (float)ys;
     fx = pin_reg(fx); fy = pin_reg(fy);
@@ -337,43 +334,48 @@ __global__ void __launch_bounds__(TILE_PX, (KT <= 8 && DP <= 4) ? SS_RASTER_MINB
         if (lane < 4) lst[cnt + lane] = 0;  // padding of the last group of 4: a readable slot, masked out below
         __syncwarp();
 
-        // float32 filter over the relevant candidates, 4 per step.  The sign bits of (d^2 - rho^2) are
-        // funnel-shifted into a 4-bit mask; a non-empty mask is pushed as one 10-bit entry
-        // [group:6 | mask:4] into a per-lane FIFO (6 entries in 64 bits).  The warp drains the FIFOs
-        // together, so the float64 path runs with most lanes active.
-        unsigned long long q = 0;
-        int qn = 0;
-        unsigned cur = 0;  // entry being consumed
-        auto drain_round = [&]() {
-            if ((cur & 15u) == 0u && qn > 0) { --qn; cur = (unsigned)(q >> (10 * qn)) & 0x3ffu; }
-            if (cur & 15u) {
-                const int bit = 31 - __clz((int)(cur & 15u));  // candidate u of the group sits at bit 3 - u
-                const int j = lst[(int)((cur >> 4) << 2) + (3 - bit)];
-                cur &= ~(1u << bit);
-                process(j);
-            }
-        };
-        for (int k = 0; k < cnt; k += 4) {
-            const unsigned idx4 = *reinterpret_cast<const unsigned *>(lst + k);
-            unsigned acc = 0;
+        // float32 filter: every lane tests its pixel against a group of 32 relevant candidates and keeps the
+        // outcome as one 32-bit word (candidate i of the group at bit 31 - i; the sign bit of d^2 - rho^2 is
+        // funnel-shifted in).  Two such words form a 64-bit window; a lane always takes its oldest pending
+        // hit (count-leading-zeros), so lanes with few hits in the older group run ahead into the newer one
+        // while the busy lanes catch up, and the divergent float64 path runs with most lanes active.
+        auto filter_group = [&](int g) -> unsigned {
+            const int n = min(32, cnt - g);
+            unsigned w = 0;
+            int k = 0;
+#pragma unroll 2
+            for (; k < n; k += 4) {
+                const unsigned idx4 = *reinterpret_cast<const unsigned *>(lst + g + k);
 #pragma unroll
-            for (int u = 0; u < 4; ++u) {
-                const float4 c = s_cf[(idx4 >> (8 * u)) & 0xffu];
-                const float dx = fx - c.x, dy = fy - c.y;
-                const float sgn = fmaf(dx, dx, dy * dy) - c.z;  // negative = inside the bounding circle
-                acc = __funnelshift_l(__float_as_uint(sgn), acc, 1);
-            }
-            acc &= (cnt - k >= 4) ? 15u : ((0xF0u >> (cnt - k)) & 15u);
-            if (acc) { q = (q << 10) | (unsigned long long)(((unsigned)k << 2) | acc); ++qn; }
-            if (__any_sync(0xffffffffu, qn >= 6)) {
-                while (true) {
-                    const unsigned act = __ballot_sync(0xffffffffu, qn > 0 || (cur & 15u));
-                    if (__popc(act) < DRAIN_MIN_ACTIVE && !__any_sync(0xffffffffu, qn >= 6)) break;
-                    drain_round();
+                for (int u = 0; u < 4; ++u) {
+                    const float4 c = s_cf[(idx4 >> (8 * u)) & 0xffu];
+                    const float dx = fx - c.x, dy = fy - c.y;
+                    const float sgn = fmaf(dx, dx, fmaf(dy, dy, -c.z));  // negative = inside the bounding circle
+                    w = __funnelshift_l(__float_as_uint(sgn), w, 1);
                 }
             }
+            // k = n rounded up to 4: candidate i sits at bit k - 1 - i; left-align and drop the padding
+            w <<= (32 - k);
+            w &= 0xffffffffu << (32 - n);
+            return w;
+        };
+        unsigned long long win = 0;  // [older group : newer group]
+        int gbase = 0;               // list position of the older group
+        auto drain_round = [&]() {
+            if (win) {
+                const int i = __clzll((long long)win);
+                win &= ~(0x8000000000000000ull >> i);
+                process(lst[gbase + i]);
+            }
+        };
+        win = (unsigned long long)filter_group(0) << 32;
+        for (int g = 32; g < cnt; g += 32) {
+            win |= filter_group(g);
+            while (__any_sync(0xffffffffu, (unsigned)(win >> 32) != 0u)) drain_round();
+            win <<= 32;
+            gbase = g;
         }
-        while (__any_sync(0xffffffffu, qn > 0 || (cur & 15u))) drain_round();
+        while (__any_sync(0xffffffffu, win != 0ull)) drain_round();
     }
 
     // finalise, raster.py:401-414

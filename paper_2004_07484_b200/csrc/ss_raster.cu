@@ -145,16 +145,21 @@ constexpr float kLn2 = 0.6931471805599453f;
 #define SS_RASTER_MINB (SS_TOPK_SHARED ? 4 : 3)  // resident CTAs per SM the register allocation targets (d <= 4, K <= 8)
 #endif
 
+// floats per staged hit record: 12 + features, padded so that the stride is not a multiple of 8 words (records
+// would otherwise start in only 2 or 4 distinct bank groups and the divergent 128-bit loads would serialise)
+template <int DP>
+constexpr int rec_stride() { return (12 + ((DP + 3) & ~3)) % 8 == 0 ? 16 + ((DP + 3) & ~3) : 12 + ((DP + 3) & ~3); }
+
 template <int DP, int KT, int MODE>
 __global__ void __launch_bounds__(TILE_PX, (KT <= 8 && DP <= 4) ? SS_RASTER_MINB : 1) k_raster(RasterArgs a) {
     constexpr int CAP = SS_MAX_CHUNK;
     extern __shared__ __align__(16) unsigned char smem_raw[];
+    constexpr int RS = rec_stride<DP>();           // floats per staged candidate
     float4 *s_cf = (float4 *)smem_raw;            // float32 filter: centre (ortho: cx, cy, -), widened r^2
-    float4 *s_misc = s_cf + CAP;                   // r, clamped opacity o, o / gamma * log2(e), sphere id bits
-    double *s_cx = (double *)(s_misc + CAP);       // float64 centre and |c|^2 for the exact decision
-    double *s_cy = s_cx + CAP, *s_cz = s_cy + CAP, *s_n2 = s_cz + CAP;
-    float *s_f = (float *)(s_n2 + CAP);            // features, DP per candidate
-    unsigned char *s_wmask = (unsigned char *)(s_f + CAP * DP);  // per candidate: which warps' pixel blocks it can touch
+    // hit record, one per candidate, read with 128-bit loads by the divergent hit path:
+    // [cx, cy] [cz, |c|^2] (float64) [r, clamped opacity o, o / gamma * log2(e), sphere id bits] [features]
+    float *s_rec = (float *)(s_cf + CAP);
+    unsigned char *s_wmask = (unsigned char *)(s_rec + CAP * RS);  // per candidate: which warps' pixel blocks it can touch
     unsigned char *s_list = s_wmask + CAP;         // per warp: compacted indices of its relevant candidates
     constexpr int LSTRIDE = CAP + 4;
     __shared__ float4 s_rect[8];                   // per warp: sensor-space rectangle of its pixel centres
@@ -234,19 +239,22 @@ __global__ void __launch_bounds__(TILE_PX, (KT <= 8 && DP <= 4) ? SS_RASTER_MINB
 
     // exact hit evaluation for one queued candidate (reference raster.py:307-324, :380-399)
     auto process = [&](int j) {
+        const float *rp = s_rec + j * RS;
+        const double2 cxy = *reinterpret_cast<const double2 *>(rp);
+        const double2 czn = *reinterpret_cast<const double2 *>(rp + 4);
         double t, dist2, zeta;
         if (MODE == SS_MODE_PINHOLE) {
-            t = ux * s_cx[j] + uy * s_cy[j] + uz * s_cz[j];
-            dist2 = s_n2[j] - t * t;
+            t = ux * cxy.x + uy * cxy.y + uz * czn.x;
+            dist2 = czn.y - t * t;
             dist2 = dist2 < 0.0 ? 0.0 : dist2;
             zeta = t * uz;
         } else {
-            t = s_cz[j];
-            const double dx = s_cx[j] - xs, dy = s_cy[j] - ys;
+            t = czn.x;
+            const double dx = cxy.x - xs, dy = cxy.y - ys;
             dist2 = dx * dx + dy * dy;
             zeta = t;
         }
-        const float4 mi = s_misc[j];
+        const float4 mi = *reinterpret_cast<const float4 *>(rp + 8);
         const float rf = mi.x;
         const double rr = (double)rf * (double)rf;
         const double hc2 = rr - dist2;
@@ -271,7 +279,13 @@ __global__ void __launch_bounds__(TILE_PX, (KT <= 8 && DP <= 4) ? SS_RASTER_MINB
         const float term = oc * ex2_approx(x2);
         denom += term;
 #pragma unroll
-        for (int i = 0; i < DP; ++i) num[i] = fmaf(term, s_f[j * DP + i], num[i]);
+        for (int i4 = 0; i4 < DP; i4 += 4) {
+            const float4 f = *reinterpret_cast<const float4 *>(rp + 12 + i4);
+            num[i4] = fmaf(term, f.x, num[i4]);
+            if (i4 + 1 < DP) num[i4 + 1] = fmaf(term, f.y, num[i4 + 1]);
+            if (i4 + 2 < DP) num[i4 + 2] = fmaf(term, f.z, num[i4 + 2]);
+            if (i4 + 3 < DP) num[i4 + 3] = fmaf(term, f.w, num[i4 + 3]);
+        }
         // store rule term > 0 (raster.py:389) as the float64 reference sees it: float32 (FTZ)
         // underflows ~950 binary orders earlier than float64, so re-derive it in the log domain
         bool store = term > 0.0f;
@@ -286,8 +300,10 @@ __global__ void __launch_bounds__(TILE_PX, (KT <= 8 && DP <= 4) ? SS_RASTER_MINB
             const int sid = a.pair_id[s0 + start + tid];
             const Rec rc = a.rec[sid];
             const double n2 = rc.cx * rc.cx + rc.cy * rc.cy + rc.cz * rc.cz;
-            s_cx[tid] = rc.cx; s_cy[tid] = rc.cy; s_cz[tid] = rc.cz; s_n2[tid] = n2;
-            s_misc[tid] = make_float4(rc.r, rc.o, rc.o * inv_g2, __int_as_float(sid));
+            float *rp = s_rec + tid * RS;
+            *reinterpret_cast<double2 *>(rp) = make_double2(rc.cx, rc.cy);
+            *reinterpret_cast<double2 *>(rp + 4) = make_double2(rc.cz, n2);
+            *reinterpret_cast<float4 *>(rp + 8) = make_float4(rc.r, rc.o, rc.o * inv_g2, __int_as_float(sid));
             const float4 fc = a.flt[sid];  // screen-space filter record (k_project)
             s_cf[tid] = fc;
             // which warps can this candidate touch?  Same arithmetic as the per-pixel test, applied to the
@@ -304,12 +320,12 @@ __global__ void __launch_bounds__(TILE_PX, (KT <= 8 && DP <= 4) ? SS_RASTER_MINB
             s_wmask[tid] = (unsigned char)wm;
             const float *f = a.feat + (size_t)sid * a.d;
 #pragma unroll
-            for (int i = 0; i < DP; ++i) s_f[tid * DP + i] = i < a.d ? f[i] : 0.0f;
+            for (int i = 0; i < ((DP + 3) & ~3); ++i) rp[12 + i] = i < a.d ? f[i] : 0.0f;
         }
         __syncthreads();
         if (a.tau_on) {  // vote, raster.py:364-368
-            const double e0 = (MODE == SS_MODE_PINHOLE) ? sqrt(s_n2[0]) - (double)s_misc[0].x
-                                                       : s_cz[0] - (double)s_misc[0].x;
+            const double2 czn0 = *reinterpret_cast<const double2 *>(s_rec + 4);
+            const double e0 = (MODE == SS_MODE_PINHOLE) ? sqrt(czn0.y) - (double)s_rec[8] : czn0.x - (double)s_rec[8];
             const double zb = (far_ - fmin(fmax(e0 * tile_cos, near_), far_)) * inv_range;
             const double z_stop = a.gamma * (a.log_tau + (double)((m2 + log2f(denom)) * kLn2));
             if (!done && zb < z_stop) {
@@ -435,7 +451,7 @@ __global__ void __launch_bounds__(TILE_PX, (KT <= 8 && DP <= 4) ? SS_RASTER_MINB
 
 template <int DP, int KT>
 constexpr size_t raster_smem_bytes() {
-    return (size_t)SS_MAX_CHUNK * (16 + 16 + 32 + 4 * DP) + SS_MAX_CHUNK + 8 * (SS_MAX_CHUNK + 4) +
+    return (size_t)SS_MAX_CHUNK * (16 + 4 * rec_stride<DP>()) + SS_MAX_CHUNK + 8 * (SS_MAX_CHUNK + 4) +
            ((SS_TOPK_SHARED != 0 && KT <= 8) ? (size_t)KT * TILE_PX * 16 : 0);
 }
 

@@ -33,6 +33,9 @@ struct RasterArgs {
     const float *bg;
     int d, K, chunk;
     double gamma, eps_over_g, log_tau;
+    // float32 depth used for the blend exponent and as a pre-filter of the top-K (the float64 depth is only
+    // formed for hits that can enter the record): far, far - near, 1 / (far - near), error pad of the pre-filter
+    float far_f, fmn_f, inv_range_f, zpad;
     int tau_on, store_buffer, collect_stats;
     float *image, *bg_weight;
     int *ids; float *z, *clos, *log_denom;
@@ -57,8 +60,9 @@ struct TopK {
     __device__ __forceinline__ double get_z(int k) const { return z[k]; }
     __device__ __forceinline__ int get_id(int k) const { return id[k]; }
     __device__ __forceinline__ float get_c(int k) const { return c[k]; }
+    __device__ __forceinline__ bool may_enter(float) const { return true; }
     // keep the KT largest by (z desc, id asc) -- raster.py:389-399
-    __device__ __forceinline__ void insert(double zz, int sid, float cl) {
+    __device__ __forceinline__ void insert(double zz, int sid, float cl, float) {
         if (!(zz > z[KT - 1] || (zz == z[KT - 1] && sid < id[KT - 1]))) return;
         z[KT - 1] = zz; id[KT - 1] = sid; c[KT - 1] = cl;
         if (KT <= 8) {
@@ -91,6 +95,7 @@ template <int KT>
 struct TopKShared {
     double *z; int *id; float *c;  // this thread's column: slot k at [k * TILE_PX]
     double wz; int wid;            // cached slot KT-1
+    float wlo;                     // (float)wz - pad: a float32 depth below this cannot enter the record
     __device__ __forceinline__ void bind(unsigned char *base, int tid) {
         z = (double *)base + tid;
         id = (int *)(base + (size_t)KT * TILE_PX * 8) + tid;
@@ -99,9 +104,10 @@ struct TopKShared {
     __device__ __forceinline__ void init() {
 #pragma unroll
         for (int k = 0; k < KT; ++k) { z[k * TILE_PX] = -INFINITY; id[k * TILE_PX] = -1; c[k * TILE_PX] = 0.0f; }
-        wz = -INFINITY; wid = -1;
+        wz = -INFINITY; wid = -1; wlo = -INFINITY;
     }
-    __device__ __forceinline__ void insert(double zz, int sid, float cl) {
+    __device__ __forceinline__ bool may_enter(float zzf) const { return zzf >= wlo; }
+    __device__ __forceinline__ void insert(double zz, int sid, float cl, float pad) {
         if (!(zz > wz || (zz == wz && sid < wid))) return;
         int k = KT - 1;
         while (k > 0) {
@@ -113,6 +119,7 @@ struct TopKShared {
         }
         z[k * TILE_PX] = zz; id[k * TILE_PX] = sid; c[k * TILE_PX] = cl;
         wz = z[(KT - 1) * TILE_PX]; wid = id[(KT - 1) * TILE_PX];
+        wlo = (float)wz - pad;
     }
     __device__ __forceinline__ double get_z(int k) const { return z[k * TILE_PX]; }
     __device__ __forceinline__ int get_id(int k) const { return id[k * TILE_PX]; }
@@ -128,9 +135,14 @@ __device__ __forceinline__ float ex2_approx(float x) {
     asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
     return y;
 }
-__device__ __forceinline__ float sqrt_approx(float x) {
+__device__ __forceinline__ float rsqrt_approx(float x) {
     float y;
-    asm("sqrt.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+    asm("rsqrt.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+    return y;
+}
+__device__ __forceinline__ float rcp_approx(float x) {
+    float y;
+    asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
     return y;
 }
 // keeps a value in a register: stops the compiler from re-deriving it (e.g. re-converting the
@@ -190,6 +202,7 @@ __global__ void __launch_bounds__(TILE_PX, (KT <= 8 && DP <= 4) ? SS_RASTER_MINB
     // gets a NaN coordinate so it never passes (arithmetic NaNs are canonical 0x7fffffff: sign bit
     // clear, also against an infinite rho^2, where a huge finite coordinate would still pass)
     const float kFar = __int_as_float(0x7fffffff);
+    const float uzf = (float)uz;
     float fx = valid ? (float)xs : kFar;
     float fy = (float)ys;
     fx = pin_reg(fx); fy = pin_reg(fy);
@@ -258,39 +271,47 @@ __global__ void __launch_bounds__(TILE_PX, (KT <= 8 && DP <= 4) ? SS_RASTER_MINB
         const float rf = mi.x;
         const double rr = (double)rf * (double)rf;
         const double hc2 = rr - dist2;
-        if (!(hc2 > 0.0)) return;                        // dist2 < r^2
-        if (!(t > 0.0) && !(t + sqrt(hc2) > 0.0)) return;  // t + half_chord > 0
-        ++n_hits;
-        double zc = zeta < near_ ? near_ : zeta;
-        zc = zc > far_ ? far_ : zc;
-        const double zz = (far_ - zc) * inv_range;
-        // closeness 1 - dist/r as (r^2 - dist^2) / (r (r + dist)): no cancellation near the rim
-        const float cl = __fdividef((float)hc2, rf * (rf + sqrt_approx((float)dist2)));
-        const float e2 = (float)zz * mi.z;
-        if (e2 > m2) {  // online form of raster.py:382-387
-            const float sc = ex2_approx(m2 - e2);
-            denom *= sc;
+        // dist2 < r^2 and t + half_chord > 0
+        if (hc2 > 0.0 && (t > 0.0 || t + sqrt(hc2) > 0.0)) {
+            ++n_hits;
+            // float32 NDC depth for the blend exponent: (far - clip(zeta)) / (far - near)
+            const float zeta_f = (MODE == SS_MODE_PINHOLE) ? (float)t * uzf : (float)t;
+            const float zzf = fmaxf(fminf(a.far_f - zeta_f, a.fmn_f), 0.0f) * a.inv_range_f;
+            // closeness 1 - dist/r as (r^2 - dist^2) / (r (r + dist)): no cancellation near the rim
+            const float d2f = (float)dist2;
+            const float cl = (float)hc2 * rcp_approx(rf * fmaf(d2f, rsqrt_approx(fmaxf(d2f, 1e-37f)), rf));
+            const float e2 = zzf * mi.z;
+            if (e2 > m2) {  // online form of raster.py:382-387
+                const float sc = ex2_approx(m2 - e2);
+                denom *= sc;
 #pragma unroll
-            for (int i = 0; i < DP; ++i) num[i] *= sc;
-            m2 = e2;
-        }
-        const float oc = mi.y * cl;
-        const float x2 = e2 - m2;
-        const float term = oc * ex2_approx(x2);
-        denom += term;
+                for (int i = 0; i < DP; ++i) num[i] *= sc;
+                m2 = e2;
+            }
+            const float oc = mi.y * cl;
+            const float x2 = e2 - m2;
+            const float term = oc * ex2_approx(x2);
+            denom += term;
 #pragma unroll
-        for (int i4 = 0; i4 < DP; i4 += 4) {
-            const float4 f = *reinterpret_cast<const float4 *>(rp + 12 + i4);
-            num[i4] = fmaf(term, f.x, num[i4]);
-            if (i4 + 1 < DP) num[i4 + 1] = fmaf(term, f.y, num[i4 + 1]);
-            if (i4 + 2 < DP) num[i4 + 2] = fmaf(term, f.z, num[i4 + 2]);
-            if (i4 + 3 < DP) num[i4 + 3] = fmaf(term, f.w, num[i4 + 3]);
+            for (int i4 = 0; i4 < DP; i4 += 4) {
+                const float4 f = *reinterpret_cast<const float4 *>(rp + 12 + i4);
+                num[i4] = fmaf(term, f.x, num[i4]);
+                if (i4 + 1 < DP) num[i4 + 1] = fmaf(term, f.y, num[i4 + 1]);
+                if (i4 + 2 < DP) num[i4 + 2] = fmaf(term, f.z, num[i4 + 2]);
+                if (i4 + 3 < DP) num[i4 + 3] = fmaf(term, f.w, num[i4 + 3]);
+            }
+            if (top.may_enter(zzf)) {  // else: below the record's worst depth even allowing for float32 error
+                // store rule term > 0 (raster.py:389) as the float64 reference sees it: float32 (FTZ)
+                // underflows ~950 binary orders earlier than float64, so re-derive it in the log domain
+                bool store = term > 0.0f;
+                if (!store && oc > 0.0f) store = x2 + log2f(oc) > -1075.0f;
+                if (store) {
+                    double zc = zeta < near_ ? near_ : zeta;
+                    zc = zc > far_ ? far_ : zc;
+                    top.insert((far_ - zc) * inv_range, __float_as_int(mi.w), cl, a.zpad);
+                }
+            }
         }
-        // store rule term > 0 (raster.py:389) as the float64 reference sees it: float32 (FTZ)
-        // underflows ~950 binary orders earlier than float64, so re-derive it in the log domain
-        bool store = term > 0.0f;
-        if (!store && oc > 0.0f) store = x2 + log2f(oc) > -1075.0f;
-        if (store) top.insert(zz, __float_as_int(mi.w), cl);
     };
 
     for (int start = 0; start < n_cand; start += a.chunk) {
@@ -502,6 +523,12 @@ cudaError_t launch_raster(const FwdLaunch &a, cudaStream_t s) {
     r.gamma = a.gamma; r.eps_over_g = a.blend.eps / a.gamma;
     r.tau_on = a.blend.tau > 0.0 ? 1 : 0;
     r.log_tau = r.tau_on ? log(a.blend.tau / (1.0 - a.blend.tau)) : 0.0;
+    r.far_f = (float)a.cam.far_;
+    r.fmn_f = (float)(a.cam.far_ - a.cam.near_);
+    r.inv_range_f = (float)a.cam.inv_range;
+    // |float32 depth - float64 depth| <= ~6 roundings of (|far| + |zeta|) / (far - near); padded 4x
+    r.zpad = (float)(24.0 * ldexp(1.0, -24) * (fabs(a.cam.far_) + fabs(a.cam.near_) + (a.cam.far_ - a.cam.near_)) *
+                     a.cam.inv_range);
     r.store_buffer = (a.blend.flags & SS_OPT_STORE_BUFFER) ? 1 : 0;
     r.collect_stats = (a.blend.flags & SS_OPT_COLLECT_STATS) ? 1 : 0;
     r.image = a.image; r.bg_weight = a.bg_weight;

@@ -237,6 +237,89 @@ int ss_fit_step(const SsFitStepArgs *args, void *stream);
 int ss_adam_flat(float *params, const float *grads, float *m, float *v, int64_t n, double lr, double beta1,
                  double beta2, double adam_eps, int64_t step, int use_floor, double floor_value, void *stream);
 
+/* ------------------------------------------------------------------------------------------------
+ * scene surgery on the device (the sphere set changes between steps).
+ *
+ *   ss_prune_mask    <- prune's keep mask            optim.py:161-175
+ *   ss_compact_rows  <- scene.positions[keep] ... and states[name].take(keep)   optim.py:176-183, :351-352
+ *   ss_subdivide     <- subdivide (FCC x12)          optim.py:186-213
+ * ---------------------------------------------------------------------------------------------- */
+
+/* keep[i] = clip(opa[i],0,1) >= opacity_min  &&  (background_dist <= 0 || |feat[i] - bg| >= background_dist)
+ *           && (visibility == NULL || visibility[i] > 0);  comparisons in float64 like the reference. */
+int ss_prune_mask(const float *opa, const float *feat, const float *bg, const int32_t *visibility, int64_t M,
+                  int32_t d, double opacity_min, double background_dist, uint8_t *keep, void *stream);
+
+/* One per-sphere column to compact: `row_bytes` (a multiple of 4) bytes per sphere, device pointers. */
+typedef struct SsColumn {
+    const void *src;
+    void *dst;
+    int64_t row_bytes;
+} SsColumn;
+
+int ss_compact_workspace_bytes(int64_t M, size_t *out_bytes);
+
+/* Stable compaction of up to 16 columns by `keep` (M bytes, device) into their dst buffers (capacity M
+ * rows each, must not alias src); count_out (device int64) receives the number of kept rows.  `cols` is
+ * a HOST array. */
+int ss_compact_rows(const uint8_t *keep, int64_t M, const SsColumn *cols, int32_t n_cols, void *workspace,
+                    size_t workspace_bytes, int64_t *count_out, void *stream);
+
+/* Outputs hold 12 M rows; child c of parent p is row 12 p + c (reshape(m * 12, 3), optim.py:204). */
+int ss_subdivide(const float *pos, const float *rad, const float *opa, const float *feat, int64_t M, int32_t d,
+                 double scale, float *pos_out, float *rad_out, float *opa_out, float *feat_out, void *stream);
+
+/* ------------------------------------------------------------------------------------------------
+ * the on-disk record formats straight into / out of the device SoA columns.
+ *
+ *   ss_psc1_unpack / ss_psc1_pack  <- the record block of scene_from_bytes / scene_to_bytes
+ *                                     scene.py:179-227: (5 + d) little-endian float32 per sphere
+ *                                     (position*3, radius, opacity, feature*d); `records` is a DEVICE
+ *                                     copy of that block (the 16-byte header and the background are
+ *                                     parsed on the host).
+ *   ss_convert_f64_f32 / _f32_f64  <- the <f8 Adam-moment blobs of the PSK1 checkpoint, optim.py:397-405
+ * ---------------------------------------------------------------------------------------------- */
+int ss_psc1_unpack(const void *records, int64_t M, int32_t d, float *pos, float *rad, float *opa, float *feat,
+                   void *stream);
+int ss_psc1_pack(const float *pos, const float *rad, const float *opa, const float *feat, int64_t M, int32_t d,
+                 void *records_out, void *stream);
+int ss_convert_f64_f32(const double *in, float *out, int64_t n, void *stream);
+int ss_convert_f32_f64(const float *in, double *out, int64_t n, void *stream);
+
+/* ------------------------------------------------------------------------------------------------
+ * per-pixel shading of the feature map, forward and backward (shade.py).
+ * Images are (n_pixels, channels) float32, row-major, device.
+ *
+ *   ss_shade_identity[_backward]  <- shade_identity[_backward]   shade.py:66-77   (any channel count)
+ *   ss_shade_diffuse[_backward]   <- shade_diffuse[_backward]    shade.py:84-131  ([albedo:3, normal:3])
+ *   ss_shade_linear[_backward]    <- shade_linear[_backward]     shade.py:148-171 (weight (d_in,3), bias (3),
+ *                                    d_in = d + 3 when view_dirs is given)
+ *   ss_view_directions            <- view_direction_plane        shade.py:138-142
+ * ---------------------------------------------------------------------------------------------- */
+typedef struct SsLight {
+    double direction[3]; /* pointing from the light into the scene; normalised by the library */
+    double intensity;    /* >= 0 */
+    double ambient;      /* in [0, 1] */
+} SsLight;
+
+int ss_shade_identity(const float *image, int64_t n_values, float *out, void *stream);
+int ss_shade_identity_backward(const float *image, const float *upstream, int64_t n_values, float *d_image,
+                               void *stream);
+/* `lights` is a HOST array of at most 8 lights; SS_ERR_PARAMS mirrors DirectionalLight's ValidationError. */
+int ss_shade_diffuse(const float *image, int64_t n_pixels, const SsLight *lights, int32_t n_lights, float *out,
+                     void *stream);
+int ss_shade_diffuse_backward(const float *image, const float *upstream, int64_t n_pixels, const SsLight *lights,
+                              int32_t n_lights, float *d_image, void *stream);
+/* weight, bias: device float32.  view_dirs (n_pixels, 3) or NULL. */
+int ss_shade_linear(const float *image, const float *view_dirs, int64_t n_pixels, int32_t d, const float *weight,
+                    const float *bias, float *out, void *stream);
+/* d_weight (d_in * 3) and d_bias (3): device float64, or both NULL for a frozen shader. */
+int ss_shade_linear_backward(const float *image, const float *view_dirs, int64_t n_pixels, int32_t d,
+                             const float *weight, const float *bias, const float *upstream, float *d_image,
+                             double *d_weight, double *d_bias, void *stream);
+/* out: (H, W, 3) unit view directions in the camera frame (pinhole) or (0, 0, 1) (orthographic). */
+int ss_view_directions(const SsCamera *cam, float *out, void *stream);
+
 /* Number of kernels this library has launched in this process (bench.py's gpu_launches). */
 int64_t ss_launch_count(void);
 

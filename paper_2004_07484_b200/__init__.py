@@ -12,5 +12,11 @@ from .api import SoftsphereAdapter, render_backward, render_forward
 from .engine import CameraSpec, RenderEngine, default_engine
 from .function import Renderer, SphereRender
 from .optim import AdamState, DeviceFit, FitConfig, adam_step, photometric_loss, photometric_loss_device
+from .surgery import prune, prune_device, subdivide, subdivide_device
+from .sceneio import (import_point_cloud, load_checkpoint, load_checkpoint_device, load_scene, save_checkpoint,
+                      save_checkpoint_device, save_scene, scene_from_bytes, scene_from_bytes_device, scene_to_bytes,
+                      scene_to_bytes_device)
+from .shade import (DirectionalLight, LinearShader, shade_diffuse, shade_diffuse_backward, shade_identity,
+                    shade_identity_backward, shade_linear, shade_linear_backward, view_direction_plane)
 
 __version__ = "0.1.0"

@@ -79,6 +79,14 @@ class SsFitStepArgs(C.Structure):
                 ("radius_min", C.c_double), ("lambda_od", C.c_double), ("cam", SsCamera), ("energy", _P)]
 
 
+class SsColumn(C.Structure):
+    _fields_ = [("src", _P), ("dst", _P), ("row_bytes", C.c_int64)]
+
+
+class SsLight(C.Structure):
+    _fields_ = [("direction", C.c_double * 3), ("intensity", C.c_double), ("ambient", C.c_double)]
+
+
 class SsStatus(C.Structure):
     _fields_ = [("flags", C.c_int64), ("spheres_on_sensor", C.c_int64), ("num_pairs", C.c_int64),
                 ("candidates_tested", C.c_int64), ("hits_blended", C.c_int64),
@@ -88,6 +96,10 @@ class SsStatus(C.Structure):
 
 EXPORTS = ("ss_abi_version", "ss_status_string", "ss_last_cuda_error", "ss_workspace_bytes", "ss_workspace_init",
            "ss_forward", "ss_backward", "ss_read_status", "ss_photometric_loss", "ss_fit_step", "ss_adam_flat", "ss_debug_tile_lists", "ss_launch_count",
+           "ss_prune_mask", "ss_compact_workspace_bytes", "ss_compact_rows", "ss_subdivide",
+           "ss_psc1_unpack", "ss_psc1_pack", "ss_convert_f64_f32", "ss_convert_f32_f64",
+           "ss_shade_identity", "ss_shade_identity_backward", "ss_shade_diffuse", "ss_shade_diffuse_backward",
+           "ss_shade_linear", "ss_shade_linear_backward", "ss_view_directions",
            "ss_profile_enable", "ss_profile_enable_mask", "ss_profile_collect", "ss_profile_kernel_count", "ss_profile_kernel_name")
 
 _lib = None
@@ -125,6 +137,26 @@ def load():
     lib.ss_adam_flat.restype = C.c_int
     lib.ss_adam_flat.argtypes = [C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p, C.c_int64, C.c_double, C.c_double,
                                  C.c_double, C.c_double, C.c_int64, C.c_int, C.c_double, C.c_void_p]
+    V, I64, I32, D = C.c_void_p, C.c_int64, C.c_int32, C.c_double
+    for name, argtypes in (
+            ("ss_prune_mask", [V, V, V, V, I64, I32, D, D, V, V]),
+            ("ss_compact_workspace_bytes", [I64, C.POINTER(C.c_size_t)]),
+            ("ss_compact_rows", [V, I64, C.POINTER(SsColumn), I32, V, C.c_size_t, V, V]),
+            ("ss_subdivide", [V, V, V, V, I64, I32, D, V, V, V, V, V]),
+            ("ss_psc1_unpack", [V, I64, I32, V, V, V, V, V]),
+            ("ss_psc1_pack", [V, V, V, V, I64, I32, V, V]),
+            ("ss_convert_f64_f32", [V, V, I64, V]),
+            ("ss_convert_f32_f64", [V, V, I64, V]),
+            ("ss_shade_identity", [V, I64, V, V]),
+            ("ss_shade_identity_backward", [V, V, I64, V, V]),
+            ("ss_shade_diffuse", [V, I64, C.POINTER(SsLight), I32, V, V]),
+            ("ss_shade_diffuse_backward", [V, V, I64, C.POINTER(SsLight), I32, V, V]),
+            ("ss_shade_linear", [V, V, I64, I32, V, V, V, V]),
+            ("ss_shade_linear_backward", [V, V, I64, I32, V, V, V, V, V, V, V]),
+            ("ss_view_directions", [C.POINTER(SsCamera), V, V])):
+        fn = getattr(lib, name)
+        fn.restype = C.c_int
+        fn.argtypes = argtypes
     lib.ss_read_status.restype = C.c_int
     lib.ss_read_status.argtypes = [C.c_void_p, C.POINTER(SsStatus), C.c_void_p]
     lib.ss_debug_tile_lists.restype = C.c_int

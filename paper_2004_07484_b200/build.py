@@ -12,7 +12,7 @@ from concurrent.futures import ThreadPoolExecutor
 HERE = os.path.dirname(os.path.abspath(__file__))
 CSRC = os.path.join(HERE, "csrc")
 LIB = os.path.join(CSRC, "libss_b200.so")
-SOURCES = ["ss_project.cu", "ss_raster.cu", "ss_backward.cu", "ss_optim.cu", "ss_abi.cu"]
+SOURCES = ["ss_project.cu", "ss_raster.cu", "ss_backward.cu", "ss_optim.cu", "ss_scene.cu", "ss_shade.cu", "ss_abi.cu"]
 NVCC_FLAGS = [
     "-gencode", "arch=compute_100a,code=sm_100a", "-lineinfo", "-O3", "-std=c++17",
     "-Xcompiler", "-fPIC", "--expt-relaxed-constexpr",

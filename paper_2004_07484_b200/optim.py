@@ -8,8 +8,8 @@
                                             visibility + per-group Adam with radius floor, all device resident
 
 Everything runs in the sm_100a kernels of csrc/ss_optim.cu (k_photometric, k_fit_step, k_adam_flat)
-through the C ABI; there is no CPU fallback.  Pruning, subdivision, checkpoints and the epoch
-shuffling of `fit` stay out of scope.
+through the C ABI; there is no CPU fallback.  Pruning and subdivision are
+DeviceFit.prune / DeviceFit.subdivide (surgery.py), checkpoints rank 3 (sceneio.py).
 """
 from __future__ import annotations
 
@@ -45,11 +45,32 @@ class FitConfig:
     radius_min: float = RADIUS_MIN
     normalize_grads: bool = True
     gate: bool = True
+    # blending schedule (optim.py:44-47, :72-79), pruning (:51-54) and subdivision (:55-57)
+    steps: int = 500
+    gamma_start: float = 0.1
+    gamma_end: float = 1e-4
+    prune_every: int = 0
+    prune_opacity_min: float = 0.05
+    prune_background_dist: float = 0.0
+    subdivide_at: tuple = ()
+    subdivide_scale: float = float(np.sqrt(2.0))
+    seed: int = 0
 
     def __post_init__(self):
         for name in ("lr_position", "lr_radius", "lr_opacity", "lr_feature", "lr_camera"):
             if getattr(self, name) < 0:
                 raise ConfigurationError(f"{name} must be >= 0")
+        for name in ("gamma_start", "gamma_end"):
+            g = getattr(self, name)
+            if not (1e-5 <= g <= 1.0):
+                raise ConfigurationError(f"{name} must lie in [1e-5, 1]")
+
+    def gamma_at(self, step: int) -> float:
+        """Log-interpolated gamma schedule (optim.py:72-79)."""
+        if self.steps <= 1:
+            return self.gamma_start
+        t = step / (self.steps - 1)
+        return float(np.exp((1 - t) * np.log(self.gamma_start) + t * np.log(self.gamma_end)))
 
 
 @dataclass
@@ -129,14 +150,53 @@ class DeviceFit:
         self.d = int(bg.shape[0])
         self.pos, self.rad = f32(pos, (-1, 3)), f32(rad, (-1,))
         self.opa, self.feat, self.bg = f32(opa, (-1,)), f32(feat, (-1, self.d)), f32(bg, (-1,))
+        self.energy = torch.zeros(1, dtype=torch.float64, device=dev)
+        self.last = None
+        self._reset_state()
+
+    @classmethod
+    def from_device(cls, pos, rad, opa, feat, bg, config: FitConfig = None, engine: RenderEngine = None):
+        """Adopt float32 device tensors (e.g. from sceneio.scene_from_bytes_device) without a host copy."""
+        self = cls.__new__(cls)
+        self.cfg = config or FitConfig()
+        self.engine = engine or RenderEngine(pos.device)
+        self.d = int(feat.shape[1])
+        self.pos, self.rad, self.opa, self.feat, self.bg = pos, rad, opa, feat, bg
+        self.energy = torch.zeros(1, dtype=torch.float64, device=pos.device)
+        self.last = None
+        self._reset_state()
+        return self
+
+    def _reset_state(self):
+        """Fresh Adam moments, step counts and visibility for the current sphere set (optim.py:355-363)."""
         self.m = int(self.pos.shape[0])
         z = lambda t: torch.zeros_like(t)
         self.moments = {k: (z(t), z(t)) for k, t in (("pos", self.pos), ("rad", self.rad), ("opa", self.opa),
                                                      ("feat", self.feat))}
         self.steps = [0, 0, 0, 0]
-        self.visibility = torch.zeros(self.m, dtype=torch.int32, device=dev)
-        self.energy = torch.zeros(1, dtype=torch.float64, device=dev)
-        self.last = None
+        self.visibility = torch.zeros(self.m, dtype=torch.int32, device=self.pos.device)
+
+    def prune(self):
+        """prune + states[name].take(keep) + visibility reset (optim.py:345-353), all on the device.
+        Returns the number of spheres kept."""
+        from .surgery import prune_device
+        cfg = self.cfg
+        extra = [t for k in ("pos", "rad", "opa", "feat") for t in self.moments[k]]
+        self.pos, self.rad, self.opa, self.feat, extra, _ = prune_device(
+            self.pos, self.rad, self.opa, self.feat, self.bg, self.visibility, cfg.prune_opacity_min,
+            cfg.prune_background_dist, extra)
+        self.moments = {k: (extra[2 * i], extra[2 * i + 1]) for i, k in enumerate(("pos", "rad", "opa", "feat"))}
+        self.m = int(self.pos.shape[0])
+        self.visibility = torch.zeros(self.m, dtype=torch.int32, device=self.pos.device)
+        return self.m
+
+    def subdivide(self):
+        """FCC x12 subdivision with fresh optimiser state (optim.py:355-363).  Returns the new count."""
+        from .surgery import subdivide_device
+        self.pos, self.rad, self.opa, self.feat = subdivide_device(self.pos, self.rad, self.opa, self.feat,
+                                                                   self.cfg.subdivide_scale)
+        self._reset_state()
+        return self.m
 
     def apply_gradients(self, grads: dict, cam: CameraSpec):
         """k_fit_step on the outputs of RenderEngine.backward."""

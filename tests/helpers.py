@@ -13,9 +13,9 @@ GRAD_RTOL = 1e-4
 
 
 def golden_names():
-    """Render-path fixtures (fit_step.npz is the SURVEY 8(f) fixture with its own tests)."""
+    """Render-path fixtures (fit_step.npz and extras.npz are the SURVEY 8(f) fixtures with their own tests)."""
     names = sorted(os.path.splitext(os.path.basename(p))[0] for p in glob.glob(os.path.join(GOLDEN_DIR, "*.npz")))
-    return [n for n in names if not n.startswith("fit_")]
+    return [n for n in names if not n.startswith(("fit_", "extras"))]
 
 
 def load_golden(name):

@@ -45,6 +45,10 @@ __device__ __forceinline__ float ex2_approx_f(float x) {
     return y;
 }
 
+#ifndef SS_BACKWARD_MERGE
+#define SS_BACKWARD_MERGE 1
+#endif
+
 __device__ __forceinline__ void red_add_v4(float *addr, float a, float b, float c, float d) {
 #ifdef SS_EXPERIMENT_NO_RED  // measurement only: floor of the kernel without the reductions
     if (a == 123456.f) *addr = b + c + d;
@@ -55,19 +59,16 @@ __device__ __forceinline__ void red_add_v4(float *addr, float a, float b, float 
 }
 
 // Per-hit gradient pieces for one stored slot (grad.py:110-179); accumulates into the sphere's row.
-template <int DP, int MODE>
-__device__ __forceinline__ void slot_gradient(const BackArgs &a, const Rec &rc, int id, float zk, float ck,
-                                              float E, float inv_g, const float *up, const float *fhat,
-                                              const float *f, int d, double xs, double ys, double ux, double uy,
-                                              double uz, double inv_vnorm) {
+// acoef = <upstream, f_k - f_hat> (grad.py:110) is formed by the caller.
+template <int DP, int MODE, bool MERGE = false>
+__device__ __forceinline__ void slot_gradient_acoef(const BackArgs &a, const Rec &rc, int id, float zk, float ck,
+                                                    float E, float inv_g, const float *up, float acoef, int d,
+                                                    double xs, double ys, double ux, double uy, double uz,
+                                                    double inv_vnorm) {
     const Cam &cam = a.cam;
     const float o = rc.o;
     const float ez = o * zk * inv_g;
     const float w = o * ck * E;  // E = exp(o z / gamma - log_denom), computed once per slot by the caller
-    float acoef = 0.0f;
-#pragma unroll
-    for (int i = 0; i < DP; ++i)
-        if (i < d) acoef = fmaf(up[i], f[i] - fhat[i], acoef);
     const float dl_dz = acoef * w * o * inv_g;
     const float dl_dc = acoef * o * E;
     const float dl_do = acoef * ck * E * (1.0f + ez);
@@ -116,16 +117,54 @@ __device__ __forceinline__ void slot_gradient(const BackArgs &a, const Rec &rc, 
         g_sensor = -(dl_ddist * inv_dist) * (dvx * xsf + dvy * ysf) * (float)(1.0 / cam.sensor_w);
         g_focal = 0.0f;
     }
-    float *row = a.raw + (size_t)id * a.raw_stride;
-    red_add_v4(row, gcx, gcy, gcz, d_radius);
-    red_add_v4(row + 4, dl_do, g_focal, g_sensor, 1.0f);
+    float v[8 + DP];
+    v[0] = gcx; v[1] = gcy; v[2] = gcz; v[3] = d_radius;
+    v[4] = dl_do; v[5] = g_focal; v[6] = g_sensor; v[7] = 1.0f;
 #pragma unroll
-    for (int i = 0; i < DP; i += 4) {
-        if (i < d) {  // DP is a multiple of 4 and up[] is zero beyond d
-            const float v0 = w * up[i], v1 = w * up[i + 1], v2 = w * up[i + 2], v3 = w * up[i + 3];
-            red_add_v4(row + 8 + i, v0, v1, v2, v3);
+    for (int i = 0; i < DP; ++i) v[8 + i] = w * up[i];  // up[] is zero beyond d
+  if (MERGE) {
+    // Warp-level pre-reduction: the L2 processes one 16-byte reduction per lane and instruction (15.7 M of
+    // them at C3: ~50 us of this kernel), and neighbouring pixels of the 8x4 block mostly hold the SAME
+    // sphere in a slot.  Butterfly over lane ^ 1, 2, 4, 8, 16: when both partners still carry the same
+    // sphere, the lower lane takes the sum and the upper lane retires.  Whatever is left is reduced as before.
+    // (The caller guarantees that all 32 lanes get here; lanes without a hit carry id -1.)
+    int live_id = id;
+#pragma unroll
+    for (int dlt = 1; dlt < 32; dlt <<= 1) {
+        const int other = __shfl_xor_sync(0xffffffffu, live_id, dlt);
+        const bool same = other == live_id && live_id >= 0;
+        const bool lower = (threadIdx.x & dlt) == 0;
+        if (__any_sync(0xffffffffu, same)) {
+#pragma unroll
+            for (int j = 0; j < 8 + DP; ++j) {
+                const float o = __shfl_xor_sync(0xffffffffu, v[j], dlt);
+                if (same && lower) v[j] += o;
+            }
+            if (same && !lower) live_id = -1;
         }
     }
+    if (live_id < 0) return;
+  } else {
+    if (id < 0) return;
+  }
+    float *row = a.raw + (size_t)id * a.raw_stride;
+    red_add_v4(row, v[0], v[1], v[2], v[3]);
+    red_add_v4(row + 4, v[4], v[5], v[6], v[7]);
+#pragma unroll
+    for (int i = 0; i < DP; i += 4)
+        if (i < d) red_add_v4(row + 8 + i, v[8 + i], v[9 + i], v[10 + i], v[11 + i]);
+}
+
+template <int DP, int MODE, bool MERGE = false>
+__device__ __forceinline__ void slot_gradient(const BackArgs &a, const Rec &rc, int id, float zk, float ck,
+                                              float E, float inv_g, const float *up, const float *fhat,
+                                              const float *f, int d, double xs, double ys, double ux, double uy,
+                                              double uz, double inv_vnorm) {
+    float acoef = 0.0f;
+#pragma unroll
+    for (int i = 0; i < DP; ++i)
+        if (i < d) acoef = fmaf(up[i], f[i] - fhat[i], acoef);
+    slot_gradient_acoef<DP, MODE, MERGE>(a, rc, id, zk, ck, E, inv_g, up, acoef, d, xs, ys, ux, uy, uz, inv_vnorm);
 }
 
 // KT > 0: K <= KT slots held in registers, every load of a phase issued before its first use
@@ -142,9 +181,11 @@ __global__ void __launch_bounds__(TILE_PX, (KT > 0) ? SS_BACKWARD_MINB : 1) k_ba
     const int lane = tid & 31, warp = tid >> 5;
     const int px = (tile % cam.ntx) * TILE + (((warp & 1) << 3) | (lane & 7));  // 8x4 block per warp
     const int py = (tile / cam.ntx) * TILE + (((warp >> 1) << 2) | (lane >> 3));
-    if (!(px < cam.W && py < cam.H)) return;
+    const bool valid = px < cam.W && py < cam.H;
+    constexpr bool kMerge = (SS_BACKWARD_MERGE != 0) && KT > 0;  // needs all 32 lanes in the slot loop
+    if (!kMerge && !valid) return;
     const size_t P = (size_t)cam.W * cam.H;
-    const size_t pix = (size_t)py * cam.W + px;
+    const size_t pix = valid ? (size_t)py * cam.W + px : 0;
     const int K = a.K, d = a.d;
     const int *__restrict__ ids = a.ids;
     const float *__restrict__ zb = a.z;
@@ -155,7 +196,7 @@ __global__ void __launch_bounds__(TILE_PX, (KT > 0) ? SS_BACKWARD_MINB : 1) k_ba
     if (KT > 0) {
 #pragma unroll
         for (int k = 0; k < KR; ++k) {
-            const bool in = k < K;
+            const bool in = k < K && valid;
             sid[k] = in ? ids[k * P + pix] : -1;
             zk[k] = in ? zb[k * P + pix] : 0.0f;
             ck[k] = in ? cb[k * P + pix] : 0.0f;
@@ -163,7 +204,7 @@ __global__ void __launch_bounds__(TILE_PX, (KT > 0) ? SS_BACKWARD_MINB : 1) k_ba
         bool any = false;
 #pragma unroll
         for (int k = 0; k < KR; ++k) any |= sid[k] >= 0;
-        if (!any) return;
+        if (kMerge ? !__any_sync(0xffffffffu, any) : !any) return;
     } else {
         bool any = false;
         for (int k = 0; k < K; ++k) any |= ids[k * P + pix] >= 0;
@@ -193,7 +234,11 @@ __global__ void __launch_bounds__(TILE_PX, (KT > 0) ? SS_BACKWARD_MINB : 1) k_ba
         float f[KR][DP];
 #pragma unroll
         for (int k = 0; k < KR; ++k) {
+#ifdef SS_EXPERIMENT_SMALL_GATHER  // measurement only: gathers from a cache-resident subset
+            const int id = sid[k] >= 0 ? (sid[k] & 1023) : 0;
+#else
             const int id = sid[k] >= 0 ? sid[k] : 0;
+#endif
             if (sid[k] >= 0) rc[k] = a.rec[id];
 #pragma unroll
             for (int i = 0; i < DP; ++i) f[k][i] = (sid[k] >= 0 && i < d) ? a.feat[(size_t)id * d + i] : 0.0f;
@@ -211,9 +256,9 @@ __global__ void __launch_bounds__(TILE_PX, (KT > 0) ? SS_BACKWARD_MINB : 1) k_ba
         }
 #pragma unroll
         for (int k = 0; k < KR; ++k)
-            if (sid[k] >= 0)
-                slot_gradient<DP, MODE>(a, rc[k], sid[k], zk[k], ck[k], Ek[k], inv_g, up, fhat, f[k], d, xs, ys, ux,
-                                        uy, uz, inv_vnorm);
+            if (kMerge ? __any_sync(0xffffffffu, sid[k] >= 0) : sid[k] >= 0)
+                slot_gradient<DP, MODE, kMerge>(a, rc[k], sid[k], zk[k], ck[k], Ek[k], inv_g, up, fhat, f[k], d, xs, ys,
+                                                ux, uy, uz, inv_vnorm);
     } else {
         for (int k = 0; k < K; ++k) {
             const int id = ids[k * P + pix];
@@ -239,6 +284,106 @@ __global__ void __launch_bounds__(TILE_PX, (KT > 0) ? SS_BACKWARD_MINB : 1) k_ba
                                     inv_vnorm);
         }
     }
+}
+
+// Slot-parallel variant (d <= 4): one CTA per 8x4 pixel block, one WARP per stored slot (K <= 8; more slots
+// are dealt round-robin to 8 warps).  A thread handles one (pixel, slot) pair, so it holds one record instead
+// of K (~50 registers instead of 122: 2.5x more warps in flight for a kernel that is bound by the latency of
+// its two dependent gather rounds), and every plane of the slot-major buffer is read by a full warp.  The
+// only cross-slot quantity, f_hat = sum_k w_k f_k + w_bg bg (grad.py:103-108), goes through shared memory;
+// the ray of each pixel is computed once (warp 0) and shared.
+template <int DP, int MODE>
+__global__ void __launch_bounds__(256) k_backward_sw(BackArgs a, int blocks_x) {
+    __shared__ double s_ray[32][4];          // ux, uy, uz, 1 / |v|
+    __shared__ float s_fh[8][32][DP];        // per slot-warp partial of sum_k w_k f_k
+    const Cam &cam = a.cam;
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, n_warps = blockDim.x >> 5;
+    if (blockIdx.x == 0 && tid == 0) *a.clean_tag = 0ull;  // accumulators are being written: not clean any more
+    const int bx = blockIdx.x % blocks_x, by = blockIdx.x / blocks_x;
+    const int px = bx * 8 + (lane & 7), py = by * 4 + (lane >> 3);
+    const bool valid = px < cam.W && py < cam.H;
+    const size_t P = (size_t)cam.W * cam.H;
+    const size_t pix = valid ? (size_t)py * cam.W + px : 0;
+    const int K = a.K, d = a.d;
+    const double xs = ((px + 0.5) - cam.W / 2.0) * cam.pix;
+    const double ys = ((py + 0.5) - cam.H / 2.0) * cam.pix;
+    if (warp == 0) {  // ray (camera.py:332-357)
+        double ux = 0.0, uy = 0.0, uz = 1.0, ivn = 1.0;
+        if (MODE == SS_MODE_PINHOLE) {
+            const double vn = sqrt(xs * xs + ys * ys + cam.focal * cam.focal);
+            ux = xs / vn; uy = ys / vn; uz = cam.focal / vn; ivn = 1.0 / vn;
+        }
+        s_ray[lane][0] = ux; s_ray[lane][1] = uy; s_ray[lane][2] = uz; s_ray[lane][3] = ivn;
+    }
+    // slot data of this thread (first slot held in registers; further slots of K > n_warps are re-read)
+    const int k0 = warp;
+    int sid = -1; float zk = 0.0f, ck = 0.0f;
+    if (valid && k0 < K) { sid = a.ids[k0 * P + pix]; zk = a.z[k0 * P + pix]; ck = a.clos[k0 * P + pix]; }
+    const float ld = valid ? a.log_denom[pix] : 0.0f;
+    float up[DP];
+#pragma unroll
+    for (int i = 0; i < DP; ++i) up[i] = (valid && i < d) ? a.upstream[pix * d + i] : 0.0f;
+    const float inv_g = (float)(1.0 / a.gamma);
+    const float kLog2e = 1.4426950408889634f;
+
+    // phase 1: weights and the partial of f_hat over this warp's slots
+    Rec rc; rc.cx = rc.cy = rc.cz = 0.0; rc.r = 1.0f; rc.o = 0.0f;
+    float E = 0.0f, uf = 0.0f;  // first slot: exp term and <upstream, feature>
+    float part[DP];
+#pragma unroll
+    for (int i = 0; i < DP; ++i) part[i] = 0.0f;
+    if (sid >= 0) {
+        rc = a.rec[sid];
+        float f[DP];
+#pragma unroll
+        for (int i = 0; i < DP; ++i) f[i] = i < d ? a.feat[(size_t)sid * d + i] : 0.0f;
+        E = ex2_approx_f((rc.o * zk * inv_g - ld) * kLog2e);
+        const float w = rc.o * ck * E;
+#pragma unroll
+        for (int i = 0; i < DP; ++i) { part[i] = w * f[i]; uf = fmaf(up[i], f[i], uf); }
+    }
+    for (int k = k0 + n_warps; k < K; k += n_warps) {  // K > 8 only
+        const int id = valid ? a.ids[k * P + pix] : -1;
+        if (id < 0) continue;
+        const float o = a.rec[id].o;
+        const float w = o * a.clos[k * P + pix] * ex2_approx_f((o * a.z[k * P + pix] * inv_g - ld) * kLog2e);
+#pragma unroll
+        for (int i = 0; i < DP; ++i)
+            if (i < d) part[i] = fmaf(w, a.feat[(size_t)id * d + i], part[i]);
+    }
+#pragma unroll
+    for (int i = 0; i < DP; ++i) s_fh[warp][lane][i] = part[i];
+    __syncthreads();
+    if (!valid) return;
+    // f_hat and <upstream, f_hat> (same for every slot of the pixel)
+    const float w_bg = ex2_approx_f(((float)a.eps_over_g - ld) * kLog2e);
+    float fhat[DP];
+    float ufh = 0.0f;
+#pragma unroll
+    for (int i = 0; i < DP; ++i) {
+        float v = i < d ? w_bg * a.bg[i] : 0.0f;
+        for (int w = 0; w < n_warps; ++w) v += s_fh[w][lane][i];
+        fhat[i] = v;
+        ufh = fmaf(up[i], v, ufh);
+    }
+    const double ux = s_ray[lane][0], uy = s_ray[lane][1], uz = s_ray[lane][2], ivn = s_ray[lane][3];
+    // phase 2: per-slot gradients
+    if (sid >= 0)
+        slot_gradient_acoef<DP, MODE>(a, rc, sid, zk, ck, E, inv_g, up, uf - ufh, d, xs, ys, ux, uy, uz, ivn);
+    for (int k = k0 + n_warps; k < K; k += n_warps) {
+        const int id = a.ids[k * P + pix];
+        if (id < 0) continue;
+        const Rec r2 = a.rec[id];
+        float uf2 = 0.0f;
+#pragma unroll
+        for (int i = 0; i < DP; ++i)
+            if (i < d) uf2 = fmaf(up[i], a.feat[(size_t)id * d + i], uf2);
+        const float z2 = a.z[k * P + pix];
+        const float E2 = ex2_approx_f((r2.o * z2 * inv_g - ld) * kLog2e);
+        slot_gradient_acoef<DP, MODE>(a, r2, id, z2, a.clos[k * P + pix], E2, inv_g, up, uf2 - ufh, d, xs, ys, ux, uy,
+                                      uz, ivn);
+    }
+    (void)fhat;
 }
 
 // ---- clean-accumulator protocol ---------------------------------------------------------------
@@ -398,8 +543,19 @@ void launch_bw_mode(const BackArgs &b, int n_tiles, int mode, cudaStream_t s) {
     else k_backward<DP, SS_MODE_ORTHOGRAPHIC, KT><<<n_tiles, TILE_PX, 0, s>>>(b);
 }
 
+#ifndef SS_BACKWARD_SLOT_PARALLEL
+#define SS_BACKWARD_SLOT_PARALLEL 0
+#endif
+
 template <int DP>
 void launch_bw_k(const BackArgs &b, int n_tiles, int mode, cudaStream_t s) {
+    if (SS_BACKWARD_SLOT_PARALLEL && DP <= 4) {
+        const int bxn = (b.cam.W + 7) / 8, byn = (b.cam.H + 3) / 4;
+        const int warps = b.K < 8 ? b.K : 8;
+        if (mode == SS_MODE_PINHOLE) k_backward_sw<DP, SS_MODE_PINHOLE><<<bxn * byn, warps * 32, 0, s>>>(b, bxn);
+        else k_backward_sw<DP, SS_MODE_ORTHOGRAPHIC><<<bxn * byn, warps * 32, 0, s>>>(b, bxn);
+        return;
+    }
 #ifdef SS_EXPERIMENT_BWD_LOOP
     launch_bw_mode<DP, 0>(b, n_tiles, mode, s);
 #else

@@ -224,8 +224,10 @@ __global__ void __launch_bounds__(TILE_PX, (KT > 0) ? SS_BACKWARD_MINB : 1) k_ba
     const double ys = ((py + 0.5) - cam.H / 2.0) * cam.pix;
     double ux = 0.0, uy = 0.0, uz = 1.0, inv_vnorm = 1.0;
     if (MODE == SS_MODE_PINHOLE) {
-        const double vn = sqrt(xs * xs + ys * ys + cam.focal * cam.focal);
-        ux = xs / vn; uy = ys / vn; uz = cam.focal / vn; inv_vnorm = 1.0 / vn;
+        // one reciprocal square root instead of sqrt + 4 divisions: the ray only feeds gradient VALUES here
+        // (tolerance 1e-4), and the long dependent float64 chains are what this latency-bound kernel waits on
+        inv_vnorm = rsqrt(xs * xs + ys * ys + cam.focal * cam.focal);
+        ux = xs * inv_vnorm; uy = ys * inv_vnorm; uz = cam.focal * inv_vnorm;
     }
 
     if (KT > 0) {

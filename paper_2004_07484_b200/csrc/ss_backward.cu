@@ -182,7 +182,8 @@ __global__ void __launch_bounds__(TILE_PX, (KT > 0) ? SS_BACKWARD_MINB : 1) k_ba
     const int px = (tile % cam.ntx) * TILE + (((warp & 1) << 3) | (lane & 7));  // 8x4 block per warp
     const int py = (tile / cam.ntx) * TILE + (((warp >> 1) << 2) | (lane >> 3));
     const bool valid = px < cam.W && py < cam.H;
-    constexpr bool kMerge = (SS_BACKWARD_MERGE != 0) && KT > 0;  // needs all 32 lanes in the slot loop
+    // the warp-level merge needs all 32 lanes in the slot loop; 8 + d values per butterfly step pay for small d only
+    constexpr bool kMerge = (SS_BACKWARD_MERGE != 0) && DP <= 4;
     if (!kMerge && !valid) return;
     const size_t P = (size_t)cam.W * cam.H;
     const size_t pix = valid ? (size_t)py * cam.W + px : 0;
@@ -207,8 +208,8 @@ __global__ void __launch_bounds__(TILE_PX, (KT > 0) ? SS_BACKWARD_MINB : 1) k_ba
         if (kMerge ? !__any_sync(0xffffffffu, any) : !any) return;
     } else {
         bool any = false;
-        for (int k = 0; k < K; ++k) any |= ids[k * P + pix] >= 0;
-        if (!any) return;
+        for (int k = 0; k < K; ++k) any |= valid && ids[k * P + pix] >= 0;
+        if (kMerge ? !__any_sync(0xffffffffu, any) : !any) return;
     }
     const float ld = a.log_denom[pix];
     const float inv_g = (float)(1.0 / a.gamma);
@@ -263,7 +264,7 @@ __global__ void __launch_bounds__(TILE_PX, (KT > 0) ? SS_BACKWARD_MINB : 1) k_ba
                                                 ux, uy, uz, inv_vnorm);
     } else {
         for (int k = 0; k < K; ++k) {
-            const int id = ids[k * P + pix];
+            const int id = valid ? ids[k * P + pix] : -1;
             if (id < 0) continue;
             const float o = a.rec[id].o;
             const float E = ex2_approx_f((o * zb[k * P + pix] * inv_g - ld) * 1.4426950408889634f);
@@ -274,118 +275,24 @@ __global__ void __launch_bounds__(TILE_PX, (KT > 0) ? SS_BACKWARD_MINB : 1) k_ba
                 if (i < d) fhat[i] = fmaf(w, f[i], fhat[i]);
         }
         for (int k = 0; k < K; ++k) {
-            const int id = ids[k * P + pix];
-            if (id < 0) continue;
-            const Rec rc = a.rec[id];
+            const int id = valid ? ids[k * P + pix] : -1;
+            if (kMerge ? !__any_sync(0xffffffffu, id >= 0) : id < 0) continue;
+            Rec rc; rc.cx = rc.cy = rc.cz = 0.0; rc.r = 1.0f; rc.o = 0.0f;
             float f[DP];
 #pragma unroll
-            for (int i = 0; i < DP; ++i) f[i] = i < d ? a.feat[(size_t)id * d + i] : 0.0f;
-            const float zk1 = zb[k * P + pix];
+            for (int i = 0; i < DP; ++i) f[i] = 0.0f;
+            float zk1 = 0.0f, ck1 = 0.0f;
+            if (id >= 0) {
+                rc = a.rec[id];
+#pragma unroll
+                for (int i = 0; i < DP; ++i) f[i] = i < d ? a.feat[(size_t)id * d + i] : 0.0f;
+                zk1 = zb[k * P + pix]; ck1 = cb[k * P + pix];
+            }
             const float E1 = ex2_approx_f((rc.o * zk1 * inv_g - ld) * 1.4426950408889634f);
-            slot_gradient<DP, MODE>(a, rc, id, zk1, cb[k * P + pix], E1, inv_g, up, fhat, f, d, xs, ys, ux, uy, uz,
-                                    inv_vnorm);
+            slot_gradient<DP, MODE, kMerge>(a, rc, id, zk1, ck1, E1, inv_g, up, fhat, f, d, xs, ys, ux, uy, uz,
+                                            inv_vnorm);
         }
     }
-}
-
-// Slot-parallel variant (d <= 4): one CTA per 8x4 pixel block, one WARP per stored slot (K <= 8; more slots
-// are dealt round-robin to 8 warps).  A thread handles one (pixel, slot) pair, so it holds one record instead
-// of K (~50 registers instead of 122: 2.5x more warps in flight for a kernel that is bound by the latency of
-// its two dependent gather rounds), and every plane of the slot-major buffer is read by a full warp.  The
-// only cross-slot quantity, f_hat = sum_k w_k f_k + w_bg bg (grad.py:103-108), goes through shared memory;
-// the ray of each pixel is computed once (warp 0) and shared.
-template <int DP, int MODE>
-__global__ void __launch_bounds__(256) k_backward_sw(BackArgs a, int blocks_x) {
-    __shared__ double s_ray[32][4];          // ux, uy, uz, 1 / |v|
-    __shared__ float s_fh[8][32][DP];        // per slot-warp partial of sum_k w_k f_k
-    const Cam &cam = a.cam;
-    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, n_warps = blockDim.x >> 5;
-    if (blockIdx.x == 0 && tid == 0) *a.clean_tag = 0ull;  // accumulators are being written: not clean any more
-    const int bx = blockIdx.x % blocks_x, by = blockIdx.x / blocks_x;
-    const int px = bx * 8 + (lane & 7), py = by * 4 + (lane >> 3);
-    const bool valid = px < cam.W && py < cam.H;
-    const size_t P = (size_t)cam.W * cam.H;
-    const size_t pix = valid ? (size_t)py * cam.W + px : 0;
-    const int K = a.K, d = a.d;
-    const double xs = ((px + 0.5) - cam.W / 2.0) * cam.pix;
-    const double ys = ((py + 0.5) - cam.H / 2.0) * cam.pix;
-    if (warp == 0) {  // ray (camera.py:332-357)
-        double ux = 0.0, uy = 0.0, uz = 1.0, ivn = 1.0;
-        if (MODE == SS_MODE_PINHOLE) {
-            const double vn = sqrt(xs * xs + ys * ys + cam.focal * cam.focal);
-            ux = xs / vn; uy = ys / vn; uz = cam.focal / vn; ivn = 1.0 / vn;
-        }
-        s_ray[lane][0] = ux; s_ray[lane][1] = uy; s_ray[lane][2] = uz; s_ray[lane][3] = ivn;
-    }
-    // slot data of this thread (first slot held in registers; further slots of K > n_warps are re-read)
-    const int k0 = warp;
-    int sid = -1; float zk = 0.0f, ck = 0.0f;
-    if (valid && k0 < K) { sid = a.ids[k0 * P + pix]; zk = a.z[k0 * P + pix]; ck = a.clos[k0 * P + pix]; }
-    const float ld = valid ? a.log_denom[pix] : 0.0f;
-    float up[DP];
-#pragma unroll
-    for (int i = 0; i < DP; ++i) up[i] = (valid && i < d) ? a.upstream[pix * d + i] : 0.0f;
-    const float inv_g = (float)(1.0 / a.gamma);
-    const float kLog2e = 1.4426950408889634f;
-
-    // phase 1: weights and the partial of f_hat over this warp's slots
-    Rec rc; rc.cx = rc.cy = rc.cz = 0.0; rc.r = 1.0f; rc.o = 0.0f;
-    float E = 0.0f, uf = 0.0f;  // first slot: exp term and <upstream, feature>
-    float part[DP];
-#pragma unroll
-    for (int i = 0; i < DP; ++i) part[i] = 0.0f;
-    if (sid >= 0) {
-        rc = a.rec[sid];
-        float f[DP];
-#pragma unroll
-        for (int i = 0; i < DP; ++i) f[i] = i < d ? a.feat[(size_t)sid * d + i] : 0.0f;
-        E = ex2_approx_f((rc.o * zk * inv_g - ld) * kLog2e);
-        const float w = rc.o * ck * E;
-#pragma unroll
-        for (int i = 0; i < DP; ++i) { part[i] = w * f[i]; uf = fmaf(up[i], f[i], uf); }
-    }
-    for (int k = k0 + n_warps; k < K; k += n_warps) {  // K > 8 only
-        const int id = valid ? a.ids[k * P + pix] : -1;
-        if (id < 0) continue;
-        const float o = a.rec[id].o;
-        const float w = o * a.clos[k * P + pix] * ex2_approx_f((o * a.z[k * P + pix] * inv_g - ld) * kLog2e);
-#pragma unroll
-        for (int i = 0; i < DP; ++i)
-            if (i < d) part[i] = fmaf(w, a.feat[(size_t)id * d + i], part[i]);
-    }
-#pragma unroll
-    for (int i = 0; i < DP; ++i) s_fh[warp][lane][i] = part[i];
-    __syncthreads();
-    if (!valid) return;
-    // f_hat and <upstream, f_hat> (same for every slot of the pixel)
-    const float w_bg = ex2_approx_f(((float)a.eps_over_g - ld) * kLog2e);
-    float fhat[DP];
-    float ufh = 0.0f;
-#pragma unroll
-    for (int i = 0; i < DP; ++i) {
-        float v = i < d ? w_bg * a.bg[i] : 0.0f;
-        for (int w = 0; w < n_warps; ++w) v += s_fh[w][lane][i];
-        fhat[i] = v;
-        ufh = fmaf(up[i], v, ufh);
-    }
-    const double ux = s_ray[lane][0], uy = s_ray[lane][1], uz = s_ray[lane][2], ivn = s_ray[lane][3];
-    // phase 2: per-slot gradients
-    if (sid >= 0)
-        slot_gradient_acoef<DP, MODE>(a, rc, sid, zk, ck, E, inv_g, up, uf - ufh, d, xs, ys, ux, uy, uz, ivn);
-    for (int k = k0 + n_warps; k < K; k += n_warps) {
-        const int id = a.ids[k * P + pix];
-        if (id < 0) continue;
-        const Rec r2 = a.rec[id];
-        float uf2 = 0.0f;
-#pragma unroll
-        for (int i = 0; i < DP; ++i)
-            if (i < d) uf2 = fmaf(up[i], a.feat[(size_t)id * d + i], uf2);
-        const float z2 = a.z[k * P + pix];
-        const float E2 = ex2_approx_f((r2.o * z2 * inv_g - ld) * kLog2e);
-        slot_gradient_acoef<DP, MODE>(a, r2, id, z2, a.clos[k * P + pix], E2, inv_g, up, uf2 - ufh, d, xs, ys, ux, uy,
-                                      uz, ivn);
-    }
-    (void)fhat;
 }
 
 // ---- clean-accumulator protocol ---------------------------------------------------------------
@@ -545,19 +452,8 @@ void launch_bw_mode(const BackArgs &b, int n_tiles, int mode, cudaStream_t s) {
     else k_backward<DP, SS_MODE_ORTHOGRAPHIC, KT><<<n_tiles, TILE_PX, 0, s>>>(b);
 }
 
-#ifndef SS_BACKWARD_SLOT_PARALLEL
-#define SS_BACKWARD_SLOT_PARALLEL 0
-#endif
-
 template <int DP>
 void launch_bw_k(const BackArgs &b, int n_tiles, int mode, cudaStream_t s) {
-    if (SS_BACKWARD_SLOT_PARALLEL && DP <= 4) {
-        const int bxn = (b.cam.W + 7) / 8, byn = (b.cam.H + 3) / 4;
-        const int warps = b.K < 8 ? b.K : 8;
-        if (mode == SS_MODE_PINHOLE) k_backward_sw<DP, SS_MODE_PINHOLE><<<bxn * byn, warps * 32, 0, s>>>(b, bxn);
-        else k_backward_sw<DP, SS_MODE_ORTHOGRAPHIC><<<bxn * byn, warps * 32, 0, s>>>(b, bxn);
-        return;
-    }
 #ifdef SS_EXPERIMENT_BWD_LOOP
     launch_bw_mode<DP, 0>(b, n_tiles, mode, s);
 #else

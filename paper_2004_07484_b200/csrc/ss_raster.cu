@@ -47,44 +47,37 @@ struct TopK {
     double z[KT];
     int id[KT];
     float c[KT];
+    int n;  // filled slots: a new entry starts at slot n, not at the bottom of an empty record
     __device__ __forceinline__ void init() {
-        if (KT <= 8) {
-#pragma unroll
-            for (int k = 0; k < KT; ++k) { z[k] = -INFINITY; id[k] = -1; c[k] = 0.0f; }
-        } else {  // large K: keep the arrays in (L1-cached) local memory, not 4*KT registers
+        // large K: the arrays live in (L1-cached) local memory, not in 4*KT registers
 #pragma unroll 1
-            for (int k = 0; k < KT; ++k) { z[k] = -INFINITY; id[k] = -1; c[k] = 0.0f; }
-        }
+        for (int k = 0; k < KT; ++k) { z[k] = -INFINITY; id[k] = -1; c[k] = 0.0f; }
+        n = 0;
     }
     __device__ __forceinline__ void bind(unsigned char *, int) {}
     __device__ __forceinline__ double get_z(int k) const { return z[k]; }
     __device__ __forceinline__ int get_id(int k) const { return id[k]; }
     __device__ __forceinline__ float get_c(int k) const { return c[k]; }
     __device__ __forceinline__ bool may_enter(float) const { return true; }
-    // keep the KT largest by (z desc, id asc) -- raster.py:389-399
+    // keep the KT largest by (z desc, id asc) -- raster.py:389-399.  Candidates arrive roughly front to back,
+    // so the usual case is an append at slot n (one comparison) or, once full, a rejection at slot KT - 1.
     __device__ __forceinline__ void insert(double zz, int sid, float cl, float) {
-        if (!(zz > z[KT - 1] || (zz == z[KT - 1] && sid < id[KT - 1]))) return;
-        z[KT - 1] = zz; id[KT - 1] = sid; c[KT - 1] = cl;
-        if (KT <= 8) {
-#pragma unroll
-            for (int k = KT - 1; k > 0; --k) {
-                bool up = z[k] > z[k - 1] || (z[k] == z[k - 1] && id[k] < id[k - 1]);
-                if (up) {
-                    double tz = z[k]; z[k] = z[k - 1]; z[k - 1] = tz;
-                    int ti = id[k]; id[k] = id[k - 1]; id[k - 1] = ti;
-                    float tc = c[k]; c[k] = c[k - 1]; c[k - 1] = tc;
-                }
-            }
+        int k;
+        if (n < KT) {
+            k = n++;
         } else {
-#pragma unroll 1
-            for (int k = KT - 1; k > 0; --k) {
-                bool up = z[k] > z[k - 1] || (z[k] == z[k - 1] && id[k] < id[k - 1]);
-                if (!up) break;
-                double tz = z[k]; z[k] = z[k - 1]; z[k - 1] = tz;
-                int ti = id[k]; id[k] = id[k - 1]; id[k - 1] = ti;
-                float tc = c[k]; c[k] = c[k - 1]; c[k - 1] = tc;
-            }
+            if (!(zz > z[KT - 1] || (zz == z[KT - 1] && sid < id[KT - 1]))) return;
+            k = KT - 1;
         }
+#pragma unroll 1
+        while (k > 0) {
+            const double zp = z[k - 1];
+            const int ip = id[k - 1];
+            if (!(zz > zp || (zz == zp && sid < ip))) break;
+            z[k] = zp; id[k] = ip; c[k] = c[k - 1];
+            --k;
+        }
+        z[k] = zz; id[k] = sid; c[k] = cl;
     }
 };
 

@@ -156,7 +156,7 @@ template <int DP>
 constexpr int rec_stride() { return (12 + ((DP + 3) & ~3)) % 8 == 0 ? 16 + ((DP + 3) & ~3) : 12 + ((DP + 3) & ~3); }
 
 template <int DP, int KT, int MODE>
-__global__ void __launch_bounds__(TILE_PX, (KT <= 8 && DP <= 4) ? SS_RASTER_MINB : 1) k_raster(RasterArgs a) {
+__global__ void __launch_bounds__(TILE_PX, (KT <= 8 && DP <= 4) ? SS_RASTER_MINB : (DP <= 4 ? 3 : (DP <= 16 ? 2 : 1))) k_raster(RasterArgs a) {
     constexpr int CAP = SS_MAX_CHUNK;
     extern __shared__ __align__(16) unsigned char smem_raw[];
     constexpr int RS = rec_stride<DP>();           // floats per staged candidate

@@ -235,11 +235,19 @@ __global__ void __launch_bounds__(1024) k_scan(const int *__restrict__ tile_coun
     int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
     if (tid == 0) { carry_s = 0; n_big = 0; }
     __syncthreads();
-    for (int base = 0; base < n_tiles; base += 1024) {
-        int i = base + tid;
-        const int c_small = i < n_tiles ? tile_count[i] : 0;
-        int c = c_small + (i < n_tiles ? tile_count_big[i] : 0);
-        long long v = c;
+    // 4 consecutive tiles per thread: 4096 tiles (1024 x 1024 pixels) are one pass with two barriers
+    for (int base = 0; base < n_tiles; base += 4096) {
+        const int i0 = base + tid * 4;
+        int cs[4], c[4];
+        long long v = 0;
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+            const bool in = i0 + j < n_tiles;
+            cs[j] = in ? tile_count[i0 + j] : 0;
+            c[j] = cs[j] + (in ? tile_count_big[i0 + j] : 0);
+            v += c[j];
+        }
+        const long long mine = v;
         for (int o = 1; o < 32; o <<= 1) {
             long long n = __shfl_up_sync(0xffffffffu, v, o);
             if (lane >= o) v += n;
@@ -255,12 +263,16 @@ __global__ void __launch_bounds__(1024) k_scan(const int *__restrict__ tile_coun
             warp_sums[lane] = s;
         }
         __syncthreads();
-        long long carry = carry_s;
-        long long excl = carry + (wid ? warp_sums[wid - 1] : 0) + v - c;
-        if (i < n_tiles) {
-            tile_start[i] = (int)(excl > 0x7fffffffLL ? 0x7fffffffLL : excl);
-            tile_cursor[i] = c_small;  // late claims (k_emit) go behind the pre-claimed slots
-            if (c > SORT_SMALL) big_tiles[1 + atomicAdd(&n_big, 1)] = i;
+        const long long carry = carry_s;
+        long long excl = carry + (wid ? warp_sums[wid - 1] : 0) + v - mine;
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+            if (i0 + j < n_tiles) {
+                tile_start[i0 + j] = (int)(excl > 0x7fffffffLL ? 0x7fffffffLL : excl);
+                tile_cursor[i0 + j] = cs[j];  // late claims (k_emit) go behind the pre-claimed slots
+                if (c[j] > SORT_SMALL) big_tiles[1 + atomicAdd(&n_big, 1)] = i0 + j;
+            }
+            excl += c[j];
         }
         __syncthreads();
         if (tid == 0) carry_s = carry + warp_sums[31];

@@ -5,7 +5,7 @@
 //   k_shade_diffuse[_bwd]   shade_diffuse / shade_diffuse_backward        shade.py:84-131  ([albedo:3, normal:3])
 //   k_shade_linear          shade_linear (optionally view-conditioned)    shade.py:148-157
 //   k_shade_linear_bwd      shade_linear_backward: d_features per pixel, d_weight = x^T up and d_bias = sum up
-//                           reduced per 256-pixel block in shared memory, one float64 atomic per entry and block
+//                           reduced in shared memory / registers by persistent CTAs, one float64 atomic per entry and CTA
 //                                                                         shade.py:160-171
 //   k_view_dirs             view_direction_plane                          shade.py:138-142, camera.py:332-357
 //
@@ -111,9 +111,21 @@ __global__ void __launch_bounds__(256) k_shade_linear(const float *__restrict__ 
     if (i >= n_px) return;
     float a0 = s_w[MAX_IN * 3], a1 = s_w[MAX_IN * 3 + 1], a2 = s_w[MAX_IN * 3 + 2];
     const float *x = img + i * d;
-    for (int k = 0; k < d; ++k) {
-        const float v = x[k];
-        a0 = fmaf(v, s_w[3 * k], a0); a1 = fmaf(v, s_w[3 * k + 1], a1); a2 = fmaf(v, s_w[3 * k + 2], a2);
+    if ((d & 3) == 0) {  // 128-bit loads: a pixel's row is 4 d contiguous bytes
+        for (int k = 0; k < d; k += 4) {
+            const float4 q = *reinterpret_cast<const float4 *>(x + k);
+            const float v[4] = {q.x, q.y, q.z, q.w};
+#pragma unroll
+            for (int j = 0; j < 4; ++j) {
+                a0 = fmaf(v[j], s_w[3 * (k + j)], a0); a1 = fmaf(v[j], s_w[3 * (k + j) + 1], a1);
+                a2 = fmaf(v[j], s_w[3 * (k + j) + 2], a2);
+            }
+        }
+    } else {
+        for (int k = 0; k < d; ++k) {
+            const float v = x[k];
+            a0 = fmaf(v, s_w[3 * k], a0); a1 = fmaf(v, s_w[3 * k + 1], a1); a2 = fmaf(v, s_w[3 * k + 2], a2);
+        }
     }
     if (view) {
         for (int k = 0; k < 3; ++k) {
@@ -134,45 +146,75 @@ __global__ void __launch_bounds__(256) k_shade_linear_bwd(const float *__restric
     extern __shared__ float s_dyn[];
     __shared__ float s_w[MAX_IN * 3 + 3];
     const int d_in = d + (view ? 3 : 0);
-    float *s_x = s_dyn;                   // [256][d_in]  inputs of this block's pixels
-    float *s_u = s_dyn + 256 * d_in;      // [256][3]     masked upstream
+    const int xst = d_in | 1;             // odd row stride: a thread's row starts in its own bank
+    float *s_x = s_dyn;                   // [256][xst]   inputs of this block's pixels
+    float *s_u = s_dyn + 256 * xst;       // [256][3]     masked upstream
     for (int e = threadIdx.x; e < d_in * 3; e += blockDim.x) s_w[e] = weight[e];
     if (threadIdx.x < 3) s_w[MAX_IN * 3 + threadIdx.x] = bias[threadIdx.x];
     __syncthreads();
-    const long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x;
-    const bool in = i < n_px;
-    float u0 = 0.0f, u1 = 0.0f, u2 = 0.0f;
-    float *xs = s_x + threadIdx.x * d_in;
-    if (in) {
-        float a0 = s_w[MAX_IN * 3], a1 = s_w[MAX_IN * 3 + 1], a2 = s_w[MAX_IN * 3 + 2];
-        for (int k = 0; k < d_in; ++k) {
-            const float v = k < d ? img[i * d + k] : view[i * 3 + (k - d)];
-            xs[k] = v;
-            a0 = fmaf(v, s_w[3 * k], a0); a1 = fmaf(v, s_w[3 * k + 1], a1); a2 = fmaf(v, s_w[3 * k + 2], a2);
-        }
-        u0 = in01(a0) ? up[i * 3] : 0.0f;
-        u1 = in01(a1) ? up[i * 3 + 1] : 0.0f;
-        u2 = in01(a2) ? up[i * 3 + 2] : 0.0f;
-        for (int k = 0; k < d; ++k)
-            d_img[i * d + k] = u0 * s_w[3 * k] + u1 * s_w[3 * k + 1] + u2 * s_w[3 * k + 2];
-    } else {
-        for (int k = 0; k < d_in; ++k) xs[k] = 0.0f;
-    }
-    s_u[threadIdx.x * 3] = u0; s_u[threadIdx.x * 3 + 1] = u1; s_u[threadIdx.x * 3 + 2] = u2;
-    if (!d_weight) return;
-    __syncthreads();
-    // entry (k, c) of x^T up over this block's 256 pixels; entries d_in*3 .. d_in*3+2 are the bias sums
+    // entry (k, c) of x^T up (entries d_in*3 .. +2: the bias sums), split over the 256 threads as (entry,
+    // pixel-slice) pairs.  The CTA walks its pixel blocks and keeps the partial sums in registers: one float64
+    // atomic per entry, slice and CTA at the very end (an atomic per 256-pixel block would put 16 K same-address
+    // atomics on each of the ~50 entries and the kernel would wait on the L2: measured 136 us vs 40 us).
     const int t = threadIdx.x;
-    if (t < d_in * 3 + 3) {
-        const int k = t / 3, c = t - 3 * k;
-        float acc = 0.0f;
-        if (k < d_in) {
-            for (int p = 0; p < 256; ++p) acc = fmaf(s_x[p * d_in + k], s_u[p * 3 + c], acc);
-            if (acc != 0.0f) atomicAdd(d_weight + t, (double)acc);
+    const int n_ent = d_in * 3 + 3;
+    const int slices = 256 / n_ent >= 8 ? 8 : (256 / n_ent >= 4 ? 4 : (256 / n_ent >= 2 ? 2 : 1));
+    const int ent = t / slices, sl = t - ent * slices;
+    const int ek = ent / 3, ec = ent - 3 * ek;
+    float acc = 0.0f;
+    float *xs = s_x + t * xst;
+    const long long n_blocks = (n_px + 255) / 256;
+    for (long long blk = blockIdx.x; blk < n_blocks; blk += gridDim.x) {
+        const long long i = blk * 256 + t;
+        const bool in = i < n_px;
+        float u0 = 0.0f, u1 = 0.0f, u2 = 0.0f;
+        if (in) {
+            float a0 = s_w[MAX_IN * 3], a1 = s_w[MAX_IN * 3 + 1], a2 = s_w[MAX_IN * 3 + 2];
+            const bool vec = (d & 3) == 0;
+            if (vec)
+                for (int k = 0; k < d; k += 4) {
+                    const float4 q = *reinterpret_cast<const float4 *>(img + i * d + k);
+                    xs[k] = q.x; xs[k + 1] = q.y; xs[k + 2] = q.z; xs[k + 3] = q.w;
+                }
+            for (int k = 0; k < d_in; ++k) {
+                const float v = k < d ? (vec ? xs[k] : img[i * d + k]) : view[i * 3 + (k - d)];
+                xs[k] = v;
+                a0 = fmaf(v, s_w[3 * k], a0); a1 = fmaf(v, s_w[3 * k + 1], a1); a2 = fmaf(v, s_w[3 * k + 2], a2);
+            }
+            u0 = in01(a0) ? up[i * 3] : 0.0f;
+            u1 = in01(a1) ? up[i * 3 + 1] : 0.0f;
+            u2 = in01(a2) ? up[i * 3 + 2] : 0.0f;
+            if (vec) {
+                for (int k = 0; k < d; k += 4) {
+                    float4 q;
+                    q.x = u0 * s_w[3 * k] + u1 * s_w[3 * k + 1] + u2 * s_w[3 * k + 2];
+                    q.y = u0 * s_w[3 * k + 3] + u1 * s_w[3 * k + 4] + u2 * s_w[3 * k + 5];
+                    q.z = u0 * s_w[3 * k + 6] + u1 * s_w[3 * k + 7] + u2 * s_w[3 * k + 8];
+                    q.w = u0 * s_w[3 * k + 9] + u1 * s_w[3 * k + 10] + u2 * s_w[3 * k + 11];
+                    *reinterpret_cast<float4 *>(d_img + i * d + k) = q;
+                }
+            } else {
+                for (int k = 0; k < d; ++k)
+                    d_img[i * d + k] = u0 * s_w[3 * k] + u1 * s_w[3 * k + 1] + u2 * s_w[3 * k + 2];
+            }
         } else {
-            for (int p = 0; p < 256; ++p) acc += s_u[p * 3 + c];
-            if (acc != 0.0f) atomicAdd(d_bias + c, (double)acc);
+            for (int k = 0; k < d_in; ++k) xs[k] = 0.0f;
         }
+        if (!d_weight) continue;
+        s_u[t * 3] = u0; s_u[t * 3 + 1] = u1; s_u[t * 3 + 2] = u2;
+        __syncthreads();
+        if (ent < n_ent) {
+            if (ek < d_in) {
+                for (int p = sl; p < 256; p += slices) acc = fmaf(s_x[p * xst + ek], s_u[p * 3 + ec], acc);
+            } else {
+                for (int p = sl; p < 256; p += slices) acc += s_u[p * 3 + ec];
+            }
+        }
+        __syncthreads();
+    }
+    if (d_weight && ent < n_ent && acc != 0.0f) {
+        if (ek < d_in) atomicAdd(d_weight + ent, (double)acc);
+        else atomicAdd(d_bias + ec, (double)acc);
     }
 }
 
@@ -290,8 +332,10 @@ int ss_shade_linear_backward(const float *image, const float *view_dirs, int64_t
     }
     if (n_pixels == 0) return SS_OK;
     if (!image || !weight || !bias || !upstream || !d_image) return SS_ERR_NULL;
-    const size_t smem = (size_t)256 * (d_in + 3) * sizeof(float);
-    k_shade_linear_bwd<<<(unsigned)((n_pixels + 255) / 256), 256, smem, s>>>(image, view_dirs, n_pixels, d, weight,
+    const size_t smem = (size_t)256 * ((d_in | 1) + 3) * sizeof(float);
+    const long long n_blocks = (n_pixels + 255) / 256;
+    const unsigned grid = (unsigned)(n_blocks < 148 * 4 ? n_blocks : 148 * 4);  // persistent: 4 CTAs per SM
+    k_shade_linear_bwd<<<grid, 256, smem, s>>>(image, view_dirs, n_pixels, d, weight,
                                                                               bias, upstream, d_image, d_weight,
                                                                               d_bias);
     count_launch();

@@ -171,6 +171,30 @@ def main():
                   f"lin_{tag}_out": out, f"lin_{tag}_df": d_f, f"lin_{tag}_dw": d_w, f"lin_{tag}_db": d_b})
         if use_view:
             g[f"lin_{tag}_v"] = v
+    # ---- the fit loop around the path (optim.py:228-373): reference trace / events for a small problem
+    truth = make_scene(rng, 40, 3)
+    truth.opacities = np.clip(truth.opacities, 0.3, 1.0)
+    truth.positions[:, 2] = snap(rng.uniform(8, 14, 40))
+    truth.positions[:, :2] = snap(rng.uniform(-1.6, 1.6, (40, 2)))
+    truth.radii = snap(rng.uniform(0.25, 0.6, 40))
+    cam_vecs = [[0.05, -0.02, 0.0, 0.0, 0.01, 0.0, 5.0, 2.0], [-0.3, 0.1, 0.2, 0.01, 0.04, -0.02, 5.0, 2.0]]
+    fit_cams = [camera_from_vector(v, 32, 24) for v in cam_vecs]
+    params = ss.BlendParams(gamma=0.1, epsilon=1e-2, tau=0.0, top_k=5)
+    obs = [ss_optim.Observation(image=snap(ss.render_forward(truth, c, params)[0].data), camera=c) for c in fit_cams]
+    start = truth.copy()
+    start.positions = snap(start.positions + rng.normal(size=start.positions.shape) * 0.03)
+    start.features = snap(np.clip(start.features + rng.normal(size=start.features.shape) * 0.2, 0, 1))
+    fcfg = dict(lr_position=2e-3, lr_radius=1e-3, lr_opacity=5e-3, lr_feature=2e-2, lr_camera=1e-4, steps=14,
+                gamma_start=0.2, gamma_end=0.05, epsilon=1e-2, tau=0.0, top_k=5, lambda_od=0.01, prune_every=6,
+                prune_opacity_min=0.05, subdivide_at=(8,), subdivide_scale=0.6, seed=3)
+    res = ss_optim.fit(start, obs, ss_optim.FitConfig(**fcfg))
+    g.update({"fit_pos": start.positions, "fit_rad": start.radii, "fit_opa": start.opacities, "fit_feat": start.features,
+              "fit_bg": start.background, "fit_cam_vecs": np.array(cam_vecs), "fit_img0": obs[0].image,
+              "fit_img1": obs[1].image, "fit_trace": res.trace,
+              "fit_events": np.array([[e[0], 0 if e[1] == "prune" else 1, e[2]] for e in res.events]),
+              "fit_out_count": np.array(len(res.scene)),
+              "fit_out_cam0": camera_to_vector(res.cameras[0]), "fit_out_cam1": camera_to_vector(res.cameras[1])})
+    print("reference fit: events", res.events, "trace", np.round(res.trace, 5))
     print("oracle/extras.py pinned against the reference:", len(g), "arrays")
     if not args.no_write:
         np.savez_compressed(os.path.join(GOLDEN, "extras.npz"), **g)

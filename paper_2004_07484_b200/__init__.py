@@ -11,7 +11,8 @@ from .types import (AXIS_ANGLE, ORTHOGRAPHIC, PINHOLE, SIX_D, BackwardBuffer, Bl
 from .api import SoftsphereAdapter, render_backward, render_forward
 from .engine import CameraSpec, RenderEngine, default_engine
 from .function import Renderer, SphereRender
-from .optim import AdamState, DeviceFit, FitConfig, adam_step, photometric_loss, photometric_loss_device
+from .optim import (AdamState, DeviceFit, FitConfig, FitResult, Observation, adam_step, fit, photometric_loss,
+                    photometric_loss_device)
 from .surgery import prune, prune_device, subdivide, subdivide_device
 from .sceneio import (import_point_cloud, load_checkpoint, load_checkpoint_device, load_scene, save_checkpoint,
                       save_checkpoint_device, save_scene, scene_from_bytes, scene_from_bytes_device, scene_to_bytes,

@@ -241,3 +241,92 @@ class DeviceFit:
     def check_finite(self, loss: torch.Tensor):
         if not bool(torch.isfinite(loss).all()):
             raise DivergenceError("non-finite loss")
+
+
+# --------------------------------------------------------------------------------------------------
+# The fit loop (optim.py:219-373): the caller of the render path.  Everything per sphere and per pixel stays on
+# the device (DeviceFit.step / .prune / .subdivide); what remains on the host is the loop itself: the seeded
+# epoch shuffling, the gamma schedule, the 8- or 11-value camera Adam step and the event / trace bookkeeping.
+@dataclass
+class Observation:
+    """One posed training image (optim.py:25-30)."""
+    image: np.ndarray  # (H, W, d)
+    camera: object
+
+
+@dataclass
+class FitResult:
+    scene: object
+    cameras: list
+    trace: np.ndarray  # per-step loss
+    events: list = field(default_factory=list)  # (step, kind, detail)
+
+
+def _adam_host(params, grads, state: AdamState, lr, cfg):
+    """adam_step for the camera vector (8 or 11 float64 values): host arithmetic, optim.py:142-154."""
+    state.t += 1
+    state.m = cfg.beta1 * state.m + (1.0 - cfg.beta1) * grads
+    state.v = cfg.beta2 * state.v + (1.0 - cfg.beta2) * grads * grads
+    m_hat = state.m / (1.0 - cfg.beta1 ** state.t)
+    v_hat = state.v / (1.0 - cfg.beta2 ** state.t)
+    return params - lr * m_hat / (np.sqrt(v_hat) + cfg.adam_eps)
+
+
+def fit(scene, observations, config: FitConfig, renderer=None, on_step=None, device="cuda") -> FitResult:
+    """Reference signature (optim.py:228).  `renderer` is accepted for compatibility and must be None: the
+    device pipeline IS the renderer.  on_step(step, loss, fit_state, cameras) receives the DeviceFit (device
+    tensors) instead of a host scene; FitResult.scene is downloaded once at the end."""
+    from .types import (AXIS_ANGLE, SphereScene, axis_angle_vjp, camera_from_vector, camera_to_vector,
+                        rotation_6d_vjp)
+    if renderer is not None:
+        raise ConfigurationError("the device fit loop renders with its own kernels; pass renderer=None")
+    if not observations:
+        raise ValidationError("fit needs at least one observation")
+    d = scene.feature_dim
+    for i, ob in enumerate(observations):
+        if tuple(np.shape(ob.image)) != (ob.camera.height, ob.camera.width, d):
+            raise ValidationError(f"observation {i} image shape mismatch")
+    dfit = DeviceFit(scene.positions, scene.radii, scene.opacities, scene.features, scene.background, config,
+                     device=device)
+    dev = dfit.engine.device
+    targets = [torch.from_numpy(np.ascontiguousarray(ob.image, dtype=np.float32)).to(dev) for ob in observations]
+    cameras = [ob.camera for ob in observations]
+    cam_states = [AdamState.like(camera_to_vector(c)) for c in cameras]
+    rng = np.random.default_rng(config.seed)
+    trace = np.zeros(config.steps)
+    events = []
+    seen = np.zeros(len(observations), dtype=bool)
+    order = []
+    subdivide_at = set(config.subdivide_at)
+    for step in range(config.steps):
+        if not order:
+            order = list(rng.permutation(len(observations)))
+        idx = int(order.pop(0))
+        seen[idx] = True
+        cam = cameras[idx]
+        loss_t = dfit.step(targets[idx], CameraSpec.from_camera(cam), gamma=config.gamma_at(step))
+        loss = float(loss_t.item())
+        if not np.isfinite(loss):
+            raise DivergenceError(f"non-finite loss at step {step}")
+        trace[step] = loss
+        if config.lr_camera > 0:
+            cg = dfit.last["grads"]["cam_grad"].cpu().numpy()
+            g_rot = cg[3:12].reshape(3, 3)
+            d_rot = (axis_angle_vjp(cam.rotation_param, g_rot) if cam.rotation_type == AXIS_ANGLE
+                     else rotation_6d_vjp(cam.rotation_param, g_rot))
+            gvec = np.concatenate([cg[0:3], d_rot, [cg[12], cg[13]]])
+            new_vec = _adam_host(camera_to_vector(cam), gvec, cam_states[idx], config.lr_camera, config)
+            cameras[idx] = camera_from_vector(new_vec, cam.width, cam.height, near=cam.near, far=cam.far,
+                                              mode=cam.mode)
+        if config.prune_every and (step + 1) % config.prune_every == 0 and seen.all():
+            events.append((step, "prune", dfit.prune()))
+            seen[:] = False
+        if step in subdivide_at:
+            events.append((step, "subdivide", dfit.subdivide()))
+            seen[:] = False
+        if on_step is not None:
+            on_step(step, loss, dfit, cameras)
+    f64 = lambda t: t.cpu().numpy().astype(np.float64)
+    out = SphereScene(feature_dim=d, background=np.array(scene.background, dtype=np.float64),
+                      positions=f64(dfit.pos), radii=f64(dfit.rad), opacities=f64(dfit.opa), features=f64(dfit.feat))
+    return FitResult(scene=out, cameras=cameras, trace=trace, events=events)

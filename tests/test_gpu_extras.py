@@ -258,3 +258,28 @@ def test_device_fit_prune_and_subdivide_keep_rendering(engine):
     assert not fit.moments["feat"][0].any() and fit.visibility.shape == (n,)
     loss = fit.step(target, spec)  # the enlarged scene renders and updates
     assert torch.isfinite(loss).all()
+
+
+def test_fit_loop_matches_reference_trace_and_events(engine, g):
+    """The caller of the path (optim.py:228-373): seeded epoch shuffling, gamma schedule, regulariser, four Adam
+    groups + camera Adam, prune every 6 steps, subdivision at step 8 -- against the reference's own run."""
+    import paper_2004_07484_b200 as pk
+    sc = _scene(pk, g["fit_pos"], g["fit_rad"], g["fit_opa"], g["fit_feat"], g["fit_bg"])
+    cams = [pk.camera_from_vector(v, 32, 24) for v in g["fit_cam_vecs"]]
+    obs = [pk.Observation(image=g["fit_img0"], camera=cams[0]), pk.Observation(image=g["fit_img1"], camera=cams[1])]
+    cfg = pk.FitConfig(lr_position=2e-3, lr_radius=1e-3, lr_opacity=5e-3, lr_feature=2e-2, lr_camera=1e-4, steps=14,
+                       gamma_start=0.2, gamma_end=0.05, epsilon=1e-2, tau=0.0, top_k=5, lambda_od=0.01, prune_every=6,
+                       prune_opacity_min=0.05, subdivide_at=(8,), subdivide_scale=0.6, seed=3)
+    seen_steps = []
+    res = pk.fit(sc, obs, cfg, on_step=lambda step, loss, fit_state, cameras: seen_steps.append((step, fit_state.m)))
+    want_events = [(int(s), "prune" if k == 0 else "subdivide", int(n)) for s, k, n in g["fit_events"]]
+    assert res.events == want_events  # [(5, prune, 40), (8, subdivide, 480), (11, prune, 322)]
+    assert len(res.scene) == int(g["fit_out_count"]) and seen_steps[-1] == (13, len(res.scene))
+    # float32 parameters / moments on the device against the reference's float64 loop
+    assert_close(res.trace, g["fit_trace"], 2e-4, 2e-5, "loss trace")
+    assert_close(pk.camera_to_vector(res.cameras[0]), g["fit_out_cam0"], 1e-5, 1e-6, "camera 0")
+    assert_close(pk.camera_to_vector(res.cameras[1]), g["fit_out_cam1"], 1e-5, 1e-6, "camera 1")
+    with pytest.raises(pk.ValidationError):
+        pk.fit(sc, [], cfg)
+    with pytest.raises(pk.ValidationError):
+        pk.fit(sc, [pk.Observation(image=np.zeros((3, 3, 3)), camera=cams[0])], cfg)

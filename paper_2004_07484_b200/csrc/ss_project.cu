@@ -413,6 +413,142 @@ __device__ __forceinline__ void warp_sort64(El &e0, El &e1, int lane) {
     for (int j = 16; j >= 1; j >>= 1) warp_stage(e0, e1, j, (lane & j) == 0);
 }
 
+// ---- segments of <= 512 pairs (every tile of the benchmark): the same network on ONE 32-bit word ---------
+// A (key, id) element costs three shuffles and a two-word comparison per compare-exchange.  Inside one tile the
+// order-preserving key bits span a small range, so the element is packed as
+//     [ (key - key_min) >> shift : 23 bits | position in the segment : 9 bits ],   shift = max(0, bits(range) - 23):
+// a monotone integer map of the key (no floating point), every word distinct, one shuffle and a min/max per
+// compare-exchange.  Words whose 23-bit parts tie -- a handful per frame -- are then ranked exactly inside
+// their run by the full (key, id) pair; a segment where more than a quarter of the words tie (equal depths,
+// one far outlier stretching the range) takes the 64-bit network instead.
+__device__ __forceinline__ void u_stage(unsigned &e0, unsigned &e1, int m, bool keep_min) {
+    const unsigned p0 = __shfl_xor_sync(0xffffffffu, e0, m), p1 = __shfl_xor_sync(0xffffffffu, e1, m);
+    e0 = keep_min ? min(e0, p0) : max(e0, p0);
+    e1 = keep_min ? min(e1, p1) : max(e1, p1);
+}
+__device__ __forceinline__ void u_disperse64(unsigned &e0, unsigned &e1, int lane) {
+    if (e1 < e0) { const unsigned t = e0; e0 = e1; e1 = t; }  // j = 32
+#pragma unroll
+    for (int j = 16; j >= 1; j >>= 1) u_stage(e0, e1, j, (lane & j) == 0);
+}
+__device__ __forceinline__ void u_sort64(unsigned &e0, unsigned &e1, int lane) {
+#pragma unroll
+    for (int k = 2; k <= 32; k <<= 1) {
+        u_stage(e0, e1, k - 1, (lane & (k >> 1)) == 0);
+#pragma unroll
+        for (int j = k >> 2; j >= 1; j >>= 1) u_stage(e0, e1, j, (lane & j) == 0);
+    }
+    {   // flip of the k = 64 merge: index i <-> 63 - i
+        const unsigned p1 = __shfl_xor_sync(0xffffffffu, e1, 31), p0 = __shfl_xor_sync(0xffffffffu, e0, 31);
+        e0 = min(e0, p1);
+        e1 = max(e1, p0);
+    }
+#pragma unroll
+    for (int j = 16; j >= 1; j >>= 1) u_stage(e0, e1, j, (lane & j) == 0);
+}
+
+constexpr int PACK_MAX = 512;  // 9 index bits
+
+// Sorts the segment [s0, s0 + n), n <= 512, writing pair_id in place.  keys / ids: shared staging (>= 512 entries);
+// pk: 512 words.  Returns false (nothing written) when too many packed words tie.
+__device__ bool sort_packed512(int s0, int n, int np2, const unsigned long long *__restrict__ pair_key, int *pair_id,
+                               unsigned long long *keys, int *ids, unsigned *pk) {
+    __shared__ unsigned long long s_min[8], s_max[8];
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const int n_blocks = np2 >> 6;  // <= 8: at most one 64-block per warp
+    const int i0 = (warp << 6) + lane, i1 = i0 + 32;
+    unsigned long long k0 = ~0ull, k1 = ~0ull, lo = ~0ull, hi = 0ull;
+    if (warp < n_blocks) {
+        if (i0 < n) { k0 = pair_key[s0 + i0]; keys[i0] = k0; ids[i0] = pair_id[s0 + i0]; lo = k0; hi = k0; }
+        if (i1 < n) { k1 = pair_key[s0 + i1]; keys[i1] = k1; ids[i1] = pair_id[s0 + i1]; lo = min(lo, k1); hi = max(hi, k1); }
+    }
+    for (int o = 16; o > 0; o >>= 1) {
+        lo = min(lo, __shfl_xor_sync(0xffffffffu, lo, o));
+        hi = max(hi, __shfl_xor_sync(0xffffffffu, hi, o));
+    }
+    if (lane == 0) { s_min[warp] = lo; s_max[warp] = hi; }
+    __syncthreads();
+#pragma unroll
+    for (int w = 0; w < 8; ++w) { lo = min(lo, s_min[w]); hi = max(hi, s_max[w]); }
+    const unsigned long long range = hi - lo;
+    const int bits = 64 - __clzll((long long)range);  // 0 when every key is equal
+    const int shift = bits > 23 ? bits - 23 : 0;
+    unsigned e0 = 0xffffffffu, e1 = 0xffffffffu;  // padding sorts last
+    if (warp < n_blocks) {
+        if (i0 < n) e0 = ((unsigned)((k0 - lo) >> shift) << 9) | (unsigned)i0;
+        if (i1 < n) e1 = ((unsigned)((k1 - lo) >> shift) << 9) | (unsigned)i1;
+        u_sort64(e0, e1, lane);
+        if (n_blocks > 1) { pk[i0] = e0; pk[i1] = e1; }
+    }
+    if (n_blocks > 1) {
+        __syncthreads();
+        const int half = np2 >> 1;
+        for (int k = 128; k <= np2; k <<= 1) {
+            const int hk = k >> 1;
+            for (int c = tid; c < half; c += blockDim.x) {  // flip
+                const int q = c & (hk - 1);
+                const int l = ((c - q) << 1) + q, r = ((c - q) << 1) + k - 1 - q;
+                const unsigned a = pk[l], b = pk[r];
+                if (b < a) { pk[l] = b; pk[r] = a; }
+            }
+            __syncthreads();
+            for (int j = hk >> 1; j >= 64; j >>= 1) {  // long-distance disperse stages
+                for (int c = tid; c < half; c += blockDim.x) {
+                    const int q = c & (j - 1);
+                    const int l = ((c - q) << 1) + q;
+                    const unsigned a = pk[l], b = pk[l + j];
+                    if (b < a) { pk[l] = b; pk[l + j] = a; }
+                }
+                __syncthreads();
+            }
+            if (warp < n_blocks) {  // j = 32 .. 1 in registers
+                e0 = pk[i0]; e1 = pk[i1];
+                u_disperse64(e0, e1, lane);
+                pk[i0] = e0; pk[i1] = e1;
+            }
+            __syncthreads();
+        }
+    } else {
+        if (warp == 0) { pk[i0] = e0; pk[i1] = e1; }
+        __syncthreads();
+    }
+    // pk[0 .. n) is sorted by the 23-bit part; words in a run of equal parts are ranked by (key, id)
+    int ties = 0;
+    for (int p = tid; p < n; p += blockDim.x) {
+        const unsigned q = pk[p] >> 9;
+        ties += (p > 0 && (pk[p - 1] >> 9) == q) || (p + 1 < n && (pk[p + 1] >> 9) == q);
+    }
+    int total = ties;
+    for (int o = 16; o > 0; o >>= 1) total += __shfl_xor_sync(0xffffffffu, total, o);
+    __shared__ int s_ties[8];
+    if (lane == 0) s_ties[warp] = total;
+    __syncthreads();
+    total = 0;
+#pragma unroll
+    for (int w = 0; w < 8; ++w) total += s_ties[w];
+    if (total * 4 > n) return false;
+    for (int p = tid; p < n; p += blockDim.x) {
+        const unsigned w = pk[p];
+        const unsigned q = w >> 9;
+        const int me = (int)(w & 511u);
+        int dst = p;
+        if (total > 0 && ((p > 0 && (pk[p - 1] >> 9) == q) || (p + 1 < n && (pk[p + 1] >> 9) == q))) {
+            int a = p;
+            while (a > 0 && (pk[a - 1] >> 9) == q) --a;
+            const unsigned long long km = keys[me];
+            const int im = ids[me];
+            int rank = 0;
+            for (int j = a; j < n && (pk[j] >> 9) == q; ++j) {
+                const int o = (int)(pk[j] & 511u);
+                rank += pair_less(keys[o], ids[o], km, im) ? 1 : 0;
+            }
+            dst = a + rank;
+        }
+        pair_id[s0 + dst] = ids[me];
+    }
+    return true;
+}
+
 __global__ void __launch_bounds__(256) k_tile_sort_small(const int *__restrict__ tile_start,
                                                          const unsigned long long *__restrict__ pair_key,
                                                          int *pair_id, const long long *__restrict__ status) {
@@ -424,6 +560,11 @@ __global__ void __launch_bounds__(256) k_tile_sort_small(const int *__restrict__
     if (n < 2 || n > SORT_SMALL) return;
     int np2 = 64;
     while (np2 < n) np2 <<= 1;
+    if (np2 <= PACK_MAX) {
+        __shared__ unsigned pk[PACK_MAX];
+        if (sort_packed512(s0, n, np2, pair_key, pair_id, keys, ids, pk)) return;
+        __syncthreads();  // too many ties: the 64-bit network below re-reads the untouched segment
+    }
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     const int n_blocks = np2 >> 6;
     // load straight into registers, sort each 64-block (merges k = 2..64), park in shared memory

@@ -84,3 +84,50 @@ def test_random_geometry_vs_oracle(engine, seed):
         grad_close(cg[0:3], gr["d_translation"], "d_translation", rtol=2e-4)
         grad_close(cg[3:12].reshape(3, 3), gr["grad_rot_matrix"], "dL/dR", rtol=2e-4)
         grad_close(cg[12:14], [gr["d_focal"], gr["d_sensor_width"]], "intrinsics", rtol=2e-4)
+
+
+@pytest.mark.parametrize("case", ["equal_depth_ortho", "duplicates", "outlier_range", "near_ties"])
+def test_tile_sort_tie_paths_vs_oracle(engine, case):
+    """The per-tile sort packs (key, position) into 32 bits when a segment has <= 512 pairs; these scenes force its
+    three regimes -- runs of tied 23-bit parts ranked exactly, too many ties (64-bit network instead) and a range
+    stretched by one outlier -- and the order must stay the reference's (earliest, then index)."""
+    from oracle import oracle as orc
+    from paper_2004_07484_b200 import CameraSpec, camera_from_vector
+    rng = np.random.default_rng(11)
+    m, w, h = 900, 48, 32
+    mode = "pinhole"
+    pos = np.column_stack([rng.uniform(-1.5, 1.5, m), rng.uniform(-1.0, 1.0, m), rng.uniform(8, 30, m)])
+    rad = rng.uniform(0.05, 0.4, m)
+    vec = [0, 0, 0, 0, 0, 0, 5.0, 2.0]
+    if case == "equal_depth_ortho":   # every earliest = c_z - r identical: all ties, order by index
+        mode = "orthographic"
+        vec = [0, 0, 0, 0, 0, 0, 5.0, 6.0]
+        rad = np.full(m, 0.25)
+        pos[:, 2] = 12.0
+        pos[:, :2] = rng.uniform(-2.5, 2.5, (m, 2))
+    elif case == "duplicates":        # 10 % exact duplicates: runs of two equal keys inside otherwise distinct keys
+        dup = rng.choice(m, m // 10, replace=False)
+        src = rng.choice(m, m // 10, replace=False)
+        pos[dup], rad[dup] = pos[src], rad[src]
+    elif case == "outlier_range":     # one huge far sphere in every tile: the 23-bit parts of the rest collapse
+        pos[:, 2] = rng.uniform(8.0, 8.0004, m)
+        pos[0], rad[0] = (0.0, 0.0, 4000.0), 3000.0
+    elif case == "near_ties":         # keys differing in the last float64 bits only
+        base = rng.uniform(8, 30, 30)
+        pos[:, 2] = base[rng.integers(0, 30, m)] * (1.0 + rng.integers(0, 4, m) * 2.0 ** -50)
+        pos[:, :2] = 0.0
+        rad[:] = 0.2
+    f32 = np.float32
+    pos, rad = pos.astype(f32), rad.astype(f32)
+    opa, feat, bg = rng.uniform(0.2, 1, m).astype(f32), rng.uniform(0, 1, (m, 3)).astype(f32), np.zeros(3, f32)
+    cam = camera_from_vector(vec, w, h, mode=mode)
+    ocam = orc.camera_from_vector(vec, w, h, mode=mode)
+    f = engine.forward(pos, rad, opa, feat, bg, CameraSpec.from_camera(cam), gamma=0.1, tau=0.0, top_k=5)
+    starts, ids = engine.tile_lists(m, 3, w, h, 5)
+    o_ids, o_starts = orc.tile_lists(pos, rad, ocam)
+    assert np.array_equal(starts, o_starts)
+    assert np.array_equal(ids, o_ids)
+    seg = np.diff(o_starts)
+    assert seg.max() <= 2048 and (seg > 64).any()  # exercises the multi-block packed path
+    ref = orc.render_forward(pos, rad, opa, feat, bg, ocam, gamma=0.1, tau=0.0, top_k=5)
+    assert np.array_equal(f["ids"].permute(1, 2, 0).cpu().numpy(), ref["ids"])

@@ -153,7 +153,11 @@ constexpr float kLn2 = 0.6931471805599453f;
 // floats per staged hit record: 12 + features, padded so that the stride is not a multiple of 8 words (records
 // would otherwise start in only 2 or 4 distinct bank groups and the divergent 128-bit loads would serialise)
 template <int DP>
-constexpr int rec_stride() { return (12 + ((DP + 3) & ~3)) % 8 == 0 ? 16 + ((DP + 3) & ~3) : 12 + ((DP + 3) & ~3); }
+constexpr int rec_stride() {
+    // d = 3: 48-byte record [cx, cy | cz, r, id | o, f0, f1, f2] -- |c|^2 and o/gamma are re-formed per hit
+    // (3 DFMA + 1 FMUL cost less than a fourth divergent 128-bit load)
+    return DP == 3 ? 12 : ((12 + ((DP + 3) & ~3)) % 8 == 0 ? 16 + ((DP + 3) & ~3) : 12 + ((DP + 3) & ~3));
+}
 
 template <int DP, int KT, int MODE>
 __global__ void __launch_bounds__(TILE_PX, (KT <= 8 && DP <= 4) ? SS_RASTER_MINB : (DP <= 4 ? 3 : (DP <= 16 ? 2 : 1))) k_raster(RasterArgs a) {
@@ -247,7 +251,20 @@ __global__ void __launch_bounds__(TILE_PX, (KT <= 8 && DP <= 4) ? SS_RASTER_MINB
     auto process = [&](int j) {
         const float *rp = s_rec + j * RS;
         const double2 cxy = *reinterpret_cast<const double2 *>(rp);
-        const double2 czn = *reinterpret_cast<const double2 *>(rp + 4);
+        constexpr bool kCompact = DP == 3;
+        double2 czn;
+        float4 mi;  // r, clamped opacity o, o / gamma * log2(e), sphere id bits
+        float4 f3 = make_float4(0.f, 0.f, 0.f, 0.f);
+        if (kCompact) {
+            const float4 q = *reinterpret_cast<const float4 *>(rp + 4);   // cz (float64), r, id
+            f3 = *reinterpret_cast<const float4 *>(rp + 8);                // o, f0, f1, f2
+            czn.x = __hiloint2double(__float_as_int(q.y), __float_as_int(q.x));
+            czn.y = cxy.x * cxy.x + cxy.y * cxy.y + czn.x * czn.x;
+            mi = make_float4(q.z, f3.x, f3.x * inv_g2, q.w);
+        } else {
+            czn = *reinterpret_cast<const double2 *>(rp + 4);
+            mi = *reinterpret_cast<const float4 *>(rp + 8);
+        }
         double t, dist2, zeta;
         if (MODE == SS_MODE_PINHOLE) {
             t = ux * cxy.x + uy * cxy.y + uz * czn.x;
@@ -260,7 +277,6 @@ __global__ void __launch_bounds__(TILE_PX, (KT <= 8 && DP <= 4) ? SS_RASTER_MINB
             dist2 = dx * dx + dy * dy;
             zeta = t;
         }
-        const float4 mi = *reinterpret_cast<const float4 *>(rp + 8);
         const float rf = mi.x;
         const double rr = (double)rf * (double)rf;
         const double hc2 = rr - dist2;
@@ -285,8 +301,13 @@ __global__ void __launch_bounds__(TILE_PX, (KT <= 8 && DP <= 4) ? SS_RASTER_MINB
             const float x2 = e2 - m2;
             const float term = oc * ex2_approx(x2);
             denom += term;
+            if (kCompact) {
+                num[0] = fmaf(term, f3.y, num[0]);
+                if (DP > 1) num[1 % DP] = fmaf(term, f3.z, num[1 % DP]);
+                if (DP > 2) num[2 % DP] = fmaf(term, f3.w, num[2 % DP]);
+            }
 #pragma unroll
-            for (int i4 = 0; i4 < DP; i4 += 4) {
+            for (int i4 = 0; i4 < (kCompact ? 0 : DP); i4 += 4) {
                 const float4 f = *reinterpret_cast<const float4 *>(rp + 12 + i4);
                 num[i4] = fmaf(term, f.x, num[i4]);
                 if (i4 + 1 < DP) num[i4 + 1] = fmaf(term, f.y, num[i4 + 1]);
@@ -316,8 +337,14 @@ __global__ void __launch_bounds__(TILE_PX, (KT <= 8 && DP <= 4) ? SS_RASTER_MINB
             const double n2 = rc.cx * rc.cx + rc.cy * rc.cy + rc.cz * rc.cz;
             float *rp = s_rec + tid * RS;
             *reinterpret_cast<double2 *>(rp) = make_double2(rc.cx, rc.cy);
-            *reinterpret_cast<double2 *>(rp + 4) = make_double2(rc.cz, n2);
-            *reinterpret_cast<float4 *>(rp + 8) = make_float4(rc.r, rc.o, rc.o * inv_g2, __int_as_float(sid));
+            if (DP == 3) {
+                *reinterpret_cast<float4 *>(rp + 4) = make_float4(__int_as_float(__double2loint(rc.cz)),
+                                                                  __int_as_float(__double2hiint(rc.cz)), rc.r,
+                                                                  __int_as_float(sid));
+            } else {
+                *reinterpret_cast<double2 *>(rp + 4) = make_double2(rc.cz, n2);
+                *reinterpret_cast<float4 *>(rp + 8) = make_float4(rc.r, rc.o, rc.o * inv_g2, __int_as_float(sid));
+            }
             const float4 fc = a.flt[sid];  // screen-space filter record (k_project)
             s_cf[tid] = fc;
             // which warps can this candidate touch?  Same arithmetic as the per-pixel test, applied to the
@@ -333,13 +360,23 @@ __global__ void __launch_bounds__(TILE_PX, (KT <= 8 && DP <= 4) ? SS_RASTER_MINB
             }
             s_wmask[tid] = (unsigned char)wm;
             const float *f = a.feat + (size_t)sid * a.d;
+            if (DP == 3) {
+                *reinterpret_cast<float4 *>(rp + 8) = make_float4(rc.o, f[0], a.d > 1 ? f[1] : 0.0f, a.d > 2 ? f[2] : 0.0f);
+            } else {
 #pragma unroll
-            for (int i = 0; i < ((DP + 3) & ~3); ++i) rp[12 + i] = i < a.d ? f[i] : 0.0f;
+                for (int i = 0; i < ((DP + 3) & ~3); ++i) rp[12 + i] = i < a.d ? f[i] : 0.0f;
+            }
         }
         __syncthreads();
         if (a.tau_on) {  // vote, raster.py:364-368
-            const double2 czn0 = *reinterpret_cast<const double2 *>(s_rec + 4);
-            const double e0 = (MODE == SS_MODE_PINHOLE) ? sqrt(czn0.y) - (double)s_rec[8] : czn0.x - (double)s_rec[8];
+            double2 czn0 = *reinterpret_cast<const double2 *>(s_rec + 4);  // c_z, |c|^2 (d = 3: c_z, [r, id])
+            float r0 = s_rec[8];
+            if (DP == 3) {
+                const double2 cxy0 = *reinterpret_cast<const double2 *>(s_rec);
+                r0 = s_rec[6];
+                czn0.y = cxy0.x * cxy0.x + cxy0.y * cxy0.y + czn0.x * czn0.x;
+            }
+            const double e0 = (MODE == SS_MODE_PINHOLE) ? sqrt(czn0.y) - (double)r0 : czn0.x - (double)r0;
             const double zb = (far_ - fmin(fmax(e0 * tile_cos, near_), far_)) * inv_range;
             const double z_stop = a.gamma * (a.log_tau + (double)((m2 + log2f(denom)) * kLn2));
             if (!done && zb < z_stop) {

@@ -125,25 +125,25 @@ __device__ __forceinline__ void slot_gradient_acoef(const BackArgs &a, const Rec
   if (MERGE) {
     // Warp-level pre-reduction: the L2 processes one 16-byte reduction per lane and instruction (15.7 M of
     // them at C3: ~50 us of this kernel), and neighbouring pixels of the 8x4 block mostly hold the SAME
-    // sphere in a slot.  Butterfly over lane ^ 1, 2, 4, 8, 16: when both partners still carry the same
-    // sphere, the lower lane takes the sum and the upper lane retires.  Whatever is left is reduced as before.
-    // (The caller guarantees that all 32 lanes get here; lanes without a hit carry id -1.)
-    int live_id = id;
+    // sphere in a slot.  match.any groups the lanes by sphere; the groups are summed by pointer jumping
+    // (every lane adds the partial sum of its next peer and then points to that peer's next: after
+    // log2(group size) rounds the lowest lane of each group holds the group's sum) and only that lane issues
+    // the reductions.  (The caller guarantees that all 32 lanes get here; lanes without a hit carry id -1.)
+    const unsigned lane = threadIdx.x & 31u;
+    const unsigned peers = __match_any_sync(0xffffffffu, id);
+    const unsigned above = peers & (0xfffffffeu << lane);  // peers in higher lanes
+    int nxt = above ? __ffs((int)above) - 1 : -1;
+    while (__any_sync(0xffffffffu, nxt >= 0)) {
+        const int src = nxt >= 0 ? nxt : (int)lane;
 #pragma unroll
-    for (int dlt = 1; dlt < 32; dlt <<= 1) {
-        const int other = __shfl_xor_sync(0xffffffffu, live_id, dlt);
-        const bool same = other == live_id && live_id >= 0;
-        const bool lower = (threadIdx.x & dlt) == 0;
-        if (__any_sync(0xffffffffu, same)) {
-#pragma unroll
-            for (int j = 0; j < 8 + DP; ++j) {
-                const float o = __shfl_xor_sync(0xffffffffu, v[j], dlt);
-                if (same && lower) v[j] += o;
-            }
-            if (same && !lower) live_id = -1;
+        for (int j = 0; j < 8 + DP; ++j) {
+            const float o = __shfl_sync(0xffffffffu, v[j], src);
+            if (nxt >= 0) v[j] += o;
         }
+        const int nn = __shfl_sync(0xffffffffu, nxt, src);
+        nxt = nxt >= 0 ? nn : -1;
     }
-    if (live_id < 0) return;
+    if (id < 0 || (peers & ((1u << lane) - 1u)) != 0u) return;  // not the group's lowest lane
   } else {
     if (id < 0) return;
   }

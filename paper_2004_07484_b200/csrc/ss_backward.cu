@@ -137,6 +137,7 @@ __device__ __forceinline__ void slot_gradient_acoef(const BackArgs &a, const Rec
         const int src = nxt >= 0 ? nxt : (int)lane;
 #pragma unroll
         for (int j = 0; j < 8 + DP; ++j) {
+            if (j == 7) continue;  // the pixel count is the group size (set below)
             const float o = __shfl_sync(0xffffffffu, v[j], src);
             if (nxt >= 0) v[j] += o;
         }
@@ -144,6 +145,7 @@ __device__ __forceinline__ void slot_gradient_acoef(const BackArgs &a, const Rec
         nxt = nxt >= 0 ? nn : -1;
     }
     if (id < 0 || (peers & ((1u << lane) - 1u)) != 0u) return;  // not the group's lowest lane
+    v[7] = (float)__popc(peers);
   } else {
     if (id < 0) return;
   }

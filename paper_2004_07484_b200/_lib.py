@@ -16,6 +16,7 @@ SS_ERR_WORKSPACE, SS_ERR_UNSUPPORTED, SS_ERR_CUDA = 5, 6, 7
 
 FLAG_INVALID_INPUT = 1
 FLAG_PAIR_OVERFLOW = 2
+FLAG_LIST_FALLBACK = 4
 
 OPT_STORE_BUFFER = 1
 OPT_COLLECT_STATS = 2

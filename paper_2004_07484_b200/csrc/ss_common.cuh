@@ -44,6 +44,7 @@ struct Layout {
     size_t slot4;        // M int4: slot inside each touched tile's segment (spheres touching <= 4 tiles)
     size_t proj_r;       // M double
     size_t flt;          // M float4: screen-space filter (projected centre x, y, padded rho^2, -)
+    size_t bucket;       // n_tiles x SORT_SMALL int32: sphere ids written straight into their tile by k_project
     size_t pair_key;     // max_pairs uint64
     size_t pair_id;      // max_pairs int32
     size_t raw;          // M * raw_stride float (backward accumulators)
@@ -85,6 +86,7 @@ inline Layout make_layout(const SsDims &dm) {
     L.slot4 = take(M * 16);
     L.proj_r = take(M * 8);
     L.flt = take(M * 16);
+    L.bucket = take((size_t)L.n_tiles * SORT_SMALL * 4);
     L.pair_key = take(P * 8);
     L.pair_id = take(P * 4);
     L.raw = take(M * (size_t)L.raw_stride * 4);

@@ -5,7 +5,11 @@
 //               validation (scene.py:91-114) -- float64 per sphere, M-parallel, plus the
 //               per-tile candidate COUNT (one atomic per touched tile).
 //   k_scan      exclusive prefix sum of the tile counts -> tile_start (raster.py:290-292).
-//   k_emit      writes each (tile, sphere) pair into its tile's segment.  The slot inside the
+//               k_project also writes the sphere id straight into a fixed-capacity bucket of every touched tile
+//               (2048 ids per tile; spheres touching > 4 tiles fill the bucket from its far end), so the common
+//               case needs no emit pass at all: the per-tile sort reads its bucket and gathers the keys.
+//   k_emit      (fallback, only when some tile holds more than 2048 spheres: SS_FLAG_LIST_FALLBACK)
+//               writes each (tile, sphere) pair into its tile's segment.  The slot inside the
 //               segment was already claimed by k_project's counting atomic (spheres touching
 //               <= 4 tiles, i.e. nearly all), so k_emit is a pure streaming pass; spheres that
 //               touch more tiles claim their slots here, behind the pre-claimed ones.
@@ -92,7 +96,7 @@ struct ProjectArgs {
     const float *pos, *rad, *opa, *feat, *bg;
     Cam cam;
     Rec *rec; unsigned long long *key; ushort4 *trect; double *proj_r; float4 *flt;
-    int *tile_count; int *tile_count_big; int4 *slot4; long long *status;
+    int *tile_count; int *tile_count_big; int4 *slot4; int *bucket; long long *status;
     int32_t *rect; uint8_t *on_sensor; double *earliest; double *proj_r_out;
     int records_only; int validate;
 };
@@ -167,7 +171,11 @@ __global__ void __launch_bounds__(256) k_project(ProjectArgs a) {
                         if (j < nt) sl[j] = atomicAdd(&a.tile_count[(tr.z + j / wx) * cam.ntx + tr.x + j % wx], 1);
                 } else {
                     for (int ty = tr.z; ty <= tr.w; ++ty)
-                        for (int tx = tr.x; tx <= tr.y; ++tx) atomicAdd(&a.tile_count_big[ty * cam.ntx + tx], 1);
+                        for (int tx = tr.x; tx <= tr.y; ++tx) {
+                            const int t = ty * cam.ntx + tx;
+                            const int sb = atomicAdd(&a.tile_count_big[t], 1);
+                            if (sb < SORT_SMALL) a.bucket[(size_t)t * SORT_SMALL + SORT_SMALL - 1 - sb] = (int)i;
+                        }
                 }
             }
             a.trect[i] = tr;
@@ -213,7 +221,16 @@ __global__ void __launch_bounds__(256) k_project(ProjectArgs a) {
             }
             const float rho_pad = (float)(rho * (1.0 + 1e-5) + 4e-7 * (fabs(pcx) + fabs(pcy) + cam.sensor_w));
             a.flt[i] = make_float4((float)pcx, (float)pcy, rho_pad * rho_pad * 1.000001f, 0.0f);
-            if (on && nt <= 4) a.slot4[i] = make_int4(sl[0], sl[1], sl[2], sl[3]);
+            if (on && nt <= 4) {
+                a.slot4[i] = make_int4(sl[0], sl[1], sl[2], sl[3]);
+                const int wx = tr.y - tr.x + 1;
+#pragma unroll
+                for (int j = 0; j < 4; ++j)  // the slot claimed above is the position inside the tile's bucket
+                    if (j < nt && sl[j] < SORT_SMALL) {
+                        const int ty = (j >= wx) + (j >= 2 * wx) + (j >= 3 * wx);
+                        a.bucket[(size_t)((tr.z + ty) * cam.ntx + tr.x + (j - ty * wx)) * SORT_SMALL + sl[j]] = (int)i;
+                    }
+            }
         }
     }
     if (!a.records_only) {
@@ -270,7 +287,7 @@ __global__ void __launch_bounds__(1024) k_scan(const int *__restrict__ tile_coun
             if (i0 + j < n_tiles) {
                 tile_start[i0 + j] = (int)(excl > 0x7fffffffLL ? 0x7fffffffLL : excl);
                 tile_cursor[i0 + j] = cs[j];  // late claims (k_emit) go behind the pre-claimed slots
-                if (c[j] > SORT_SMALL) big_tiles[1 + atomicAdd(&n_big, 1)] = i0 + j;
+                if (c[j] > SORT_SMALL) big_tiles[1 + atomicAdd(&n_big, 1)] = i0 + j;  // (bucket overflow, too)
             }
             excl += c[j];
         }
@@ -282,6 +299,7 @@ __global__ void __launch_bounds__(1024) k_scan(const int *__restrict__ tile_coun
         long long total = carry_s;
         tile_start[n_tiles] = (int)(total > 0x7fffffffLL ? 0x7fffffffLL : total);
         big_tiles[0] = n_big;
+        if (n_big > 0) status[ST_FLAGS] |= SS_FLAG_LIST_FALLBACK;  // some bucket overflowed: k_emit builds the lists
         status[ST_PAIRS] = total;
         if (total > max_pairs) status[ST_FLAGS] |= SS_FLAG_PAIR_OVERFLOW;
         long long enc = status[ST_FIRST_INVALID];
@@ -295,32 +313,33 @@ __global__ void __launch_bounds__(256) k_emit(long long M, const ushort4 *__rest
                                               const int *__restrict__ tile_start, int *tile_cursor,
                                               unsigned long long *pair_key, int *pair_id, int ntx,
                                               const long long *__restrict__ status) {
-    if (status[ST_FLAGS] & SS_FLAG_PAIR_OVERFLOW) return;
-    long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x;
-    if (i >= M) return;
-    ushort4 tr = trect[i];
-    if (tr.x > tr.y) return;
-    unsigned long long k = key[i];
-    const int wx = tr.y - tr.x + 1, nt = wx * (tr.w - tr.z + 1);
-    if (nt <= 4) {
-        const int4 s4 = slot4[i];
-        const int sl[4] = {s4.x, s4.y, s4.z, s4.w};
+    const long long flags = status[ST_FLAGS];
+    if ((flags & SS_FLAG_PAIR_OVERFLOW) || !(flags & SS_FLAG_LIST_FALLBACK)) return;  // the usual case: nothing to do
+    for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < M; i += (long long)gridDim.x * blockDim.x) {
+        ushort4 tr = trect[i];
+        if (tr.x > tr.y) continue;
+        unsigned long long k = key[i];
+        const int wx = tr.y - tr.x + 1, nt = wx * (tr.w - tr.z + 1);
+        if (nt <= 4) {
+            const int4 s4 = slot4[i];
+            const int sl[4] = {s4.x, s4.y, s4.z, s4.w};
 #pragma unroll
-        for (int j = 0; j < 4; ++j)
-            if (j < nt) {
-                const int pos = tile_start[(tr.z + j / wx) * ntx + tr.x + j % wx] + sl[j];
-                pair_key[pos] = k;
-                pair_id[pos] = (int)i;
-            }
-        return;
-    }
-    for (int ty = tr.z; ty <= tr.w; ++ty)
-        for (int tx = tr.x; tx <= tr.y; ++tx) {
-            int t = ty * ntx + tx;
-            int slot = tile_start[t] + atomicAdd(&tile_cursor[t], 1);
-            pair_key[slot] = k;
-            pair_id[slot] = (int)i;
+            for (int j = 0; j < 4; ++j)
+                if (j < nt) {
+                    const int pos = tile_start[(tr.z + j / wx) * ntx + tr.x + j % wx] + sl[j];
+                    pair_key[pos] = k;
+                    pair_id[pos] = (int)i;
+                }
+            continue;
         }
+        for (int ty = tr.z; ty <= tr.w; ++ty)
+            for (int tx = tr.x; tx <= tr.y; ++tx) {
+                int t = ty * ntx + tx;
+                int slot = tile_start[t] + atomicAdd(&tile_cursor[t], 1);
+                pair_key[slot] = k;
+                pair_id[slot] = (int)i;
+            }
+    }
 }
 
 // ---- per-tile sort -------------------------------------------------------------------
@@ -449,9 +468,27 @@ __device__ __forceinline__ void u_sort64(unsigned &e0, unsigned &e1, int lane) {
 
 constexpr int PACK_MAX = 512;  // 9 index bits
 
+// Where a tile's unsorted segment comes from: the tile's bucket filled by k_project (+ a gather of the
+// per-sphere keys), or -- fallback -- the pairs written by k_emit.
+struct SegSrc {
+    const unsigned long long *pair_key; const int *pair_id;  // emitted pairs, already offset to the segment
+    const int *bucket; const unsigned long long *key;        // this tile's bucket; per-sphere keys
+    int c_small;                                             // ids of spheres touching <= 4 tiles sit at the front
+    bool direct;
+    __device__ __forceinline__ void load(int i, unsigned long long &k, int &id) const {
+        if (direct) {
+            id = bucket[i < c_small ? i : SORT_SMALL - 1 - (i - c_small)];
+            k = key[id];
+        } else {
+            k = pair_key[i];
+            id = pair_id[i];
+        }
+    }
+};
+
 // Sorts the segment [s0, s0 + n), n <= 512, writing pair_id in place.  keys / ids: shared staging (>= 512 entries);
 // pk: 512 words.  Returns false (nothing written) when too many packed words tie.
-__device__ bool sort_packed512(int s0, int n, int np2, const unsigned long long *__restrict__ pair_key, int *pair_id,
+__device__ bool sort_packed512(int s0, int n, int np2, const SegSrc &src, int *pair_id,
                                unsigned long long *keys, int *ids, unsigned *pk) {
     __shared__ unsigned long long s_min[8], s_max[8];
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
@@ -459,8 +496,9 @@ __device__ bool sort_packed512(int s0, int n, int np2, const unsigned long long 
     const int i0 = (warp << 6) + lane, i1 = i0 + 32;
     unsigned long long k0 = ~0ull, k1 = ~0ull, lo = ~0ull, hi = 0ull;
     if (warp < n_blocks) {
-        if (i0 < n) { k0 = pair_key[s0 + i0]; keys[i0] = k0; ids[i0] = pair_id[s0 + i0]; lo = k0; hi = k0; }
-        if (i1 < n) { k1 = pair_key[s0 + i1]; keys[i1] = k1; ids[i1] = pair_id[s0 + i1]; lo = min(lo, k1); hi = max(hi, k1); }
+        int id0, id1;
+        if (i0 < n) { src.load(i0, k0, id0); keys[i0] = k0; ids[i0] = id0; lo = k0; hi = k0; }
+        if (i1 < n) { src.load(i1, k1, id1); keys[i1] = k1; ids[i1] = id1; lo = min(lo, k1); hi = max(hi, k1); }
     }
     for (int o = 16; o > 0; o >>= 1) {
         lo = min(lo, __shfl_xor_sync(0xffffffffu, lo, o));
@@ -551,18 +589,28 @@ __device__ bool sort_packed512(int s0, int n, int np2, const unsigned long long 
 
 __global__ void __launch_bounds__(256) k_tile_sort_small(const int *__restrict__ tile_start,
                                                          const unsigned long long *__restrict__ pair_key,
-                                                         int *pair_id, const long long *__restrict__ status) {
+                                                         int *pair_id, const int *__restrict__ bucket,
+                                                         const unsigned long long *__restrict__ key,
+                                                         const int *__restrict__ tile_cursor,
+                                                         const long long *__restrict__ status) {
     __shared__ unsigned long long keys[SORT_SMALL];
     __shared__ int ids[SORT_SMALL];
-    if (status[ST_FLAGS] & SS_FLAG_PAIR_OVERFLOW) return;
+    const long long flags = status[ST_FLAGS];
+    if (flags & SS_FLAG_PAIR_OVERFLOW) return;
     const int t = blockIdx.x;
     const int s0 = tile_start[t], n = tile_start[t + 1] - s0;
+    SegSrc src;
+    src.direct = !(flags & SS_FLAG_LIST_FALLBACK);
+    src.pair_key = pair_key + s0; src.pair_id = pair_id + s0;
+    src.bucket = bucket + (size_t)t * SORT_SMALL; src.key = key;
+    src.c_small = tile_cursor[t];
+    if (n == 1 && src.direct && threadIdx.x == 0) pair_id[s0] = src.bucket[src.c_small ? 0 : SORT_SMALL - 1];
     if (n < 2 || n > SORT_SMALL) return;
     int np2 = 64;
     while (np2 < n) np2 <<= 1;
     if (np2 <= PACK_MAX) {
         __shared__ unsigned pk[PACK_MAX];
-        if (sort_packed512(s0, n, np2, pair_key, pair_id, keys, ids, pk)) return;
+        if (sort_packed512(s0, n, np2, src, pair_id, keys, ids, pk)) return;
         __syncthreads();  // too many ties: the 64-bit network below re-reads the untouched segment
     }
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
@@ -571,8 +619,9 @@ __global__ void __launch_bounds__(256) k_tile_sort_small(const int *__restrict__
     for (int b = warp; b < n_blocks; b += 8) {
         const int i0 = (b << 6) + lane, i1 = i0 + 32;
         El e0, e1;
-        e0.k = i0 < n ? pair_key[s0 + i0] : ~0ull; e0.id = i0 < n ? pair_id[s0 + i0] : 0x7fffffff;
-        e1.k = i1 < n ? pair_key[s0 + i1] : ~0ull; e1.id = i1 < n ? pair_id[s0 + i1] : 0x7fffffff;
+        e0.k = ~0ull; e0.id = 0x7fffffff; e1.k = ~0ull; e1.id = 0x7fffffff;
+        if (i0 < n) src.load(i0, e0.k, e0.id);
+        if (i1 < n) src.load(i1, e1.k, e1.id);
         warp_sort64(e0, e1, lane);
         if (np2 == 64) {  // done: single block
             if (i0 < n) pair_id[s0 + i0] = e0.id;
@@ -664,7 +713,7 @@ cudaError_t launch_project(const FwdLaunch &a, bool records_only, cudaStream_t s
         p.trect = (ushort4 *)(ws + L.trect); p.proj_r = (double *)(ws + L.proj_r);
         p.flt = (float4 *)(ws + L.flt);
         p.tile_count = (int *)(ws + L.tile_count); p.tile_count_big = (int *)(ws + L.tile_count_big);
-        p.slot4 = (int4 *)(ws + L.slot4); p.status = (long long *)(ws + L.status);
+        p.slot4 = (int4 *)(ws + L.slot4); p.bucket = (int *)(ws + L.bucket); p.status = (long long *)(ws + L.status);
         p.rect = a.rect; p.on_sensor = a.on_sensor; p.earliest = a.earliest; p.proj_r_out = a.proj_r_out;
         p.records_only = records_only ? 1 : 0;
         p.validate = (!records_only && !(a.blend.flags & SS_OPT_SKIP_VALIDATE)) ? 1 : 0;
@@ -694,6 +743,7 @@ cudaError_t launch_binning(const FwdLaunch &a, cudaStream_t s) {
     count_launch();
     if (M > 0) {
         unsigned grid = (unsigned)((M + 255) / 256);
+        if (grid > 148 * 32) grid = 148 * 32;  // grid-stride: in the usual (bucket) case the launch is an early exit
         {
             ProfScope ps(KID_EMIT, s);
             k_emit<<<grid, 256, 0, s>>>(M, (const ushort4 *)(ws + L.trect), (const int4 *)(ws + L.slot4),
@@ -702,7 +752,8 @@ cudaError_t launch_binning(const FwdLaunch &a, cudaStream_t s) {
         }
         {
             ProfScope ps(KID_SORT_SMALL, s);
-            k_tile_sort_small<<<L.n_tiles, 256, 0, s>>>(tile_start, pair_key, pair_id, status);
+            k_tile_sort_small<<<L.n_tiles, 256, 0, s>>>(tile_start, pair_key, pair_id, (const int *)(ws + L.bucket),
+                                                        (const unsigned long long *)(ws + L.key), tile_cursor, status);
         }
         static bool attr_set = false;
         size_t big_smem = (size_t)SORT_BIG * 12;

@@ -31,7 +31,7 @@ if ROOT not in sys.path:
 
 COUNT, SIZE, TOP_K, D = 1_000_000, 1024, 5, 3
 GAMMA, EPS, TAU = 0.1, 1e-2, 0.01
-NCU_RASTER_DRAM_BYTES = 183_704_832  # one k_raster launch at this config: 120.98 MB read + 62.72 MB written (ncu, r01k)
+NCU_RASTER_DRAM_BYTES = 180_676_352  # one k_raster launch at this config: 117.48 MB read + 63.19 MB written (ncu, r01n)
 METRIC = "fwd+bwd frames/s, 1M spheres @1024^2 n_track=5 (ms/frame = ms_per_step / views_per_rank)"
 WORKLOAD = ("C3: 1M uniform 3px spheres (cli.py:_benchmark_scene, seed 0), 1024x1024, d=3, n_track=5, "
             "gamma=0.1 eps=0.01 tau=0.01, full fwd+bwd incl. camera gradients, upstream=sign(image-0.5)")
@@ -316,9 +316,9 @@ def main():
             "roofline": {"kernel": "k_raster", "bound": "hbm", "achieved": achieved, "peak": peak,
                          "unit": "GB/s", "frac": achieved / peak, "traffic": NCU_RASTER_DRAM_BYTES,
                          "traffic_source": "dram__bytes_read.sum + dram__bytes_write.sum of one k_raster launch, "
-                                           "ncu --set full, profiles/r01_summary.md (r01k)",
+                                           "ncu --set full, profiles/r01_summary.md (r01n)",
                          "issue_bound_note": "k_raster is instruction-issue bound, not HBM bound (SURVEY 8d): ncu "
-                                             "smsp__issue_active 65%, 199 M warp instructions, l1tex (shared-memory wavefronts) 77%, DRAM 8% of peak",
+                                             "smsp__issue_active 72%, 213 M warp instructions, l1tex (shared-memory wavefronts) 68%, DRAM 8% of peak",
                          "peak_source": peak_src, "algorithmic_bytes_per_launch": raster_b,
                          "avg_launch_ms": raster_ms,
                          "step": {"algorithmic_bytes_fwd": fwd_b, "algorithmic_bytes_bwd": bwd_b,

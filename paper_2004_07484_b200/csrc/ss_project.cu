@@ -168,7 +168,10 @@ __global__ void __launch_bounds__(256) k_project(ProjectArgs a) {
                 if (nt <= 4) {  // claim the slots now; k_emit needs no atomics for this sphere
 #pragma unroll
                     for (int j = 0; j < 4; ++j)
-                        if (j < nt) sl[j] = atomicAdd(&a.tile_count[(tr.z + j / wx) * cam.ntx + tr.x + j % wx], 1);
+                        if (j < nt) {  // tile j of the rectangle, row-major (no integer division: nt <= 4)
+                            const int ty = (j >= wx) + (j >= 2 * wx) + (j >= 3 * wx);
+                            sl[j] = atomicAdd(&a.tile_count[(tr.z + ty) * cam.ntx + tr.x + (j - ty * wx)], 1);
+                        }
                 } else {
                     for (int ty = tr.z; ty <= tr.w; ++ty)
                         for (int tx = tr.x; tx <= tr.y; ++tx) {

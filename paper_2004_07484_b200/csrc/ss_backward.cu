@@ -184,8 +184,8 @@ __global__ void __launch_bounds__(TILE_PX, (KT > 0) ? SS_BACKWARD_MINB : 1) k_ba
     const int px = (tile % cam.ntx) * TILE + (((warp & 1) << 3) | (lane & 7));  // 8x4 block per warp
     const int py = (tile / cam.ntx) * TILE + (((warp >> 1) << 2) | (lane >> 3));
     const bool valid = px < cam.W && py < cam.H;
-    // the warp-level merge needs all 32 lanes in the slot loop; 8 + d values per butterfly step pay for small d only
-    constexpr bool kMerge = (SS_BACKWARD_MERGE != 0) && DP <= 4;
+    // the warp-level merge needs all 32 lanes in the slot loop; it pays up to d = 16 (C5: 5.3 -> 4.8 ms), not measured beyond
+    constexpr bool kMerge = (SS_BACKWARD_MERGE != 0) && DP <= 16;
     if (!kMerge && !valid) return;
     const size_t P = (size_t)cam.W * cam.H;
     const size_t pix = valid ? (size_t)py * cam.W + px : 0;

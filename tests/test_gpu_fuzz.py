@@ -164,3 +164,39 @@ def test_bucket_and_fallback_list_paths_vs_oracle(engine, dense):
     ref = orc.render_forward(pos, rad, opa, feat, bg, ocam, gamma=0.1, tau=0.0, top_k=5)
     assert np.array_equal(f["ids"].permute(1, 2, 0).cpu().numpy(), ref["ids"])
     assert f["status"]["hits_blended"] == ref["stats"]["hits_blended"]
+
+
+@pytest.mark.parametrize("d,k", [(16, 32), (32, 64), (32, 5), (7, 64)])
+def test_feature_maps_and_long_records_vs_oracle(engine, d, k):
+    """The template corners of the raster / backward kernels: d up to 32 channels, n_track up to 64."""
+    from oracle import oracle as orc
+    from paper_2004_07484_b200 import CameraSpec, camera_from_vector
+    rng = np.random.default_rng(100 + d + k)
+    m, w, h = 400, 40, 24
+    pos, rad, opa, feat, bg = make_random_scene_d(rng, m, d)
+    vec = [0.1, 0.0, 0.0, 0.0, 0.02, 0.0, 5.0, 2.0]
+    cam, ocam = camera_from_vector(vec, w, h), orc.camera_from_vector(vec, w, h)
+    spec = CameraSpec.from_camera(cam)
+    ref = orc.render_forward(pos, rad, opa, feat, bg, ocam, gamma=0.15, tau=0.0, top_k=k)
+    f = engine.forward(pos, rad, opa, feat, bg, spec, gamma=0.15, tau=0.0, top_k=k, collect_stats=True)
+    assert np.array_equal(f["ids"].permute(1, 2, 0).cpu().numpy(), ref["ids"])
+    assert f["status"]["hits_blended"] == ref["stats"]["hits_blended"]
+    assert_close(f["image"].cpu().numpy(), ref["image"], FWD_RTOL, FWD_ATOL, "image")
+    up = rng.normal(size=ref["image"].shape).astype(np.float32)
+    out = engine.backward(pos, rad, opa, feat, bg, spec, f, up, gamma=0.15, eps=1e-2)
+    gr = orc.render_backward(pos, rad, opa, feat, bg, ocam, ref, up.astype(np.float64))
+    assert np.array_equal(out["pixel_count"].cpu().numpy(), gr["pixel_count"])
+    grad_close(out["d_pos"].cpu().numpy(), gr["d_position"], "d_position", rtol=2e-4)
+    grad_close(out["d_rad"].cpu().numpy(), gr["d_radius"], "d_radius", rtol=2e-4)
+    grad_close(out["d_opa"].cpu().numpy(), gr["d_opacity"], "d_opacity", rtol=2e-4)
+    grad_close(out["d_feat"].cpu().numpy(), gr["d_feature"], "d_feature", rtol=2e-4)
+    cg = out["cam_grad"].cpu().numpy()
+    grad_close(cg[0:3], gr["d_translation"], "d_translation", rtol=2e-4)
+    grad_close(cg[12:14], [gr["d_focal"], gr["d_sensor_width"]], "intrinsics", rtol=2e-4)
+
+
+def make_random_scene_d(rng, m, d):
+    pos = np.column_stack([rng.uniform(-2.5, 2.5, m), rng.uniform(-1.5, 1.5, m), rng.uniform(10, 30, m)])
+    f32 = np.float32
+    return (pos.astype(f32), rng.uniform(0.1, 0.8, m).astype(f32), rng.uniform(0.1, 1.0, m).astype(f32),
+            rng.uniform(0, 1, (m, d)).astype(f32), rng.uniform(0, 1, d).astype(f32))

@@ -6,7 +6,8 @@
 //                runs the ray-geometry chain in float64 (the reference's |c| ~ 40, dist ~ 0.03
 //                cancellation costs float32 2e-4 per hit).  Per-sphere sums go to an AoS row
 //                [g_center(3), d_radius | d_opacity, g_focal, g_sensor, count | d_feature(d)]
-//                with 128-bit vector reductions (red.global.add.v4.f32).
+//                with 128-bit vector reductions (red.global.add.v4.f32), after the lanes of a warp
+//                that hold the same sphere in a slot have been summed (match.any + pointer jumping).
 //   k_finalize   reference accumulate_and_normalize + gate_small_spheres (grad.py:262-320):
 //                per-sphere normalisation, rotation to world, gating, and the block-reduced
 //                camera sums (translation, dL/dR, focal, sensor) in float64.

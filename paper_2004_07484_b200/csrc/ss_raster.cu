@@ -1,9 +1,11 @@
 // Forward raster kernel for sm_100a (reference _draw_tile, raster.py:328-417).
 //
-// One 256-thread CTA per 16x16 tile, one thread per pixel.  The tile's depth-ordered
-// candidate list is streamed in batches of `chunk` (<= 256) records staged in shared memory;
-// all lanes of a warp look at the same candidate at the same time, so every shared-memory
-// read in the test loop is a broadcast.
+// One 256-thread CTA per 16x16 tile, one thread per pixel, one 8x4 pixel block per warp.  The tile's
+// depth-ordered candidate list is streamed in batches of `chunk` (<= 256) records staged in shared memory.
+// Per batch a warp (1) compacts the candidates whose bounding circle reaches its pixel block, (2) filters
+// them 32 at a time -- all lanes look at the same candidate, so the filter's shared-memory reads are
+// broadcasts -- into one bit word per lane, and (3) drains those words: every lane evaluates ITS oldest
+// pending candidate exactly, so the divergent hit path runs with most lanes busy.
 //
 // Precision plan: the float64 reference decides hits with
 // dist^2 = |c|^2 - t^2 and orders the per-pixel top-K by float64 NDC depth.  Here a cheap
@@ -11,8 +13,9 @@
 // the circle, centred on the projected sphere centre, that bounds the sphere's projected
 // outline (radius f (tan(theta + alpha) - tan(theta)), widened for float32 rounding).  Every
 // candidate that passes is re-evaluated with the reference's own float64 formula, which alone
-// decides hit / miss and produces the depth used for ordering.  The blend (online softmax of
-// Eq. 1) runs in float32.
+// decides hit / miss.  The blend (online softmax of Eq. 1) runs in float32 on a float32 depth; the
+// float64 depth that ORDERS the top-K record is only formed for hits that pass a float32 pre-filter
+// against the record's worst entry (padded by 4x the float32 error), i.e. for hits that can enter it.
 #include <math.h>
 
 #include <type_traits>

@@ -50,7 +50,7 @@ extern "C" {
 /* ---- device-side status flags (status[0], read with ss_read_status) ---- */
 #define SS_FLAG_INVALID_INPUT 1u  /* NaN/Inf field or radius <= 0 (ValidationError, scene.py:91-114) */
 #define SS_FLAG_PAIR_OVERFLOW 2u  /* tile-sphere pairs > dims.max_pairs; nothing was drawn */
-#define SS_FLAG_LIST_FALLBACK 4u  /* informational: a tile held more than 2048 spheres, the tile lists were built by
+#define SS_FLAG_LIST_FALLBACK 4u  /* informational: a tile held more than 4096 spheres, the tile lists were built by
                                      the two-pass path (count, scan, emit) instead of the direct per-tile buckets */
 
 /* ---- option flags ---- */

@@ -44,7 +44,7 @@ struct Layout {
     size_t slot4;        // M int4: slot inside each touched tile's segment (spheres touching <= 4 tiles)
     size_t proj_r;       // M double
     size_t flt;          // M float4: screen-space filter (projected centre x, y, padded rho^2, -)
-    size_t bucket;       // n_tiles x SORT_SMALL int32: sphere ids written straight into their tile by k_project
+    size_t bucket;       // n_tiles x BUCKET_CAP int32: sphere ids written straight into their tile by k_project
     size_t pair_key;     // max_pairs uint64
     size_t pair_id;      // max_pairs int32
     size_t raw;          // M * raw_stride float (backward accumulators)
@@ -57,6 +57,7 @@ constexpr int TILE = SS_TILE;
 constexpr int TILE_PX = TILE * TILE;
 constexpr int SORT_SMALL = 2048;  // per-tile lists up to this length sort in 24 KB static smem
 constexpr int SORT_BIG = 8192;    // up to this length in 96 KB dynamic smem; beyond: in global memory
+constexpr int BUCKET_CAP = 4096;  // sphere ids per tile bucket; a fuller tile switches the frame to the emit path
 constexpr int CAM_BLOCKS_MAX = 1024;
 constexpr int CAM_VALS = 16;  // sum sc (3), G (9), focal, sensor, 2 pad
 
@@ -86,7 +87,7 @@ inline Layout make_layout(const SsDims &dm) {
     L.slot4 = take(M * 16);
     L.proj_r = take(M * 8);
     L.flt = take(M * 16);
-    L.bucket = take((size_t)L.n_tiles * SORT_SMALL * 4);
+    L.bucket = take((size_t)L.n_tiles * BUCKET_CAP * 4);
     L.pair_key = take(P * 8);
     L.pair_id = take(P * 4);
     L.raw = take(M * (size_t)L.raw_stride * 4);

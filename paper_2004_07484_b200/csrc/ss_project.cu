@@ -6,9 +6,9 @@
 //               per-tile candidate COUNT (one atomic per touched tile).
 //   k_scan      exclusive prefix sum of the tile counts -> tile_start (raster.py:290-292).
 //               k_project also writes the sphere id straight into a fixed-capacity bucket of every touched tile
-//               (2048 ids per tile; spheres touching > 4 tiles fill the bucket from its far end), so the common
+//               (4096 ids per tile; spheres touching > 4 tiles fill the bucket from its far end), so the common
 //               case needs no emit pass at all: the per-tile sort reads its bucket and gathers the keys.
-//   k_emit      (fallback, only when some tile holds more than 2048 spheres: SS_FLAG_LIST_FALLBACK)
+//   k_emit      (fallback, only when some tile holds more than 4096 spheres: SS_FLAG_LIST_FALLBACK)
 //               writes each (tile, sphere) pair into its tile's segment.  The slot inside the
 //               segment was already claimed by k_project's counting atomic (spheres touching
 //               <= 4 tiles, i.e. nearly all), so k_emit is a pure streaming pass; spheres that
@@ -177,7 +177,7 @@ __global__ void __launch_bounds__(256) k_project(ProjectArgs a) {
                         for (int tx = tr.x; tx <= tr.y; ++tx) {
                             const int t = ty * cam.ntx + tx;
                             const int sb = atomicAdd(&a.tile_count_big[t], 1);
-                            if (sb < SORT_SMALL) a.bucket[(size_t)t * SORT_SMALL + SORT_SMALL - 1 - sb] = (int)i;
+                            if (sb < BUCKET_CAP) a.bucket[(size_t)t * BUCKET_CAP + BUCKET_CAP - 1 - sb] = (int)i;
                         }
                 }
             }
@@ -229,9 +229,9 @@ __global__ void __launch_bounds__(256) k_project(ProjectArgs a) {
                 const int wx = tr.y - tr.x + 1;
 #pragma unroll
                 for (int j = 0; j < 4; ++j)  // the slot claimed above is the position inside the tile's bucket
-                    if (j < nt && sl[j] < SORT_SMALL) {
+                    if (j < nt && sl[j] < BUCKET_CAP) {
                         const int ty = (j >= wx) + (j >= 2 * wx) + (j >= 3 * wx);
-                        a.bucket[(size_t)((tr.z + ty) * cam.ntx + tr.x + (j - ty * wx)) * SORT_SMALL + sl[j]] = (int)i;
+                        a.bucket[(size_t)((tr.z + ty) * cam.ntx + tr.x + (j - ty * wx)) * BUCKET_CAP + sl[j]] = (int)i;
                     }
             }
         }
@@ -251,9 +251,9 @@ __global__ void __launch_bounds__(1024) k_scan(const int *__restrict__ tile_coun
                                                long long max_pairs, long long M, long long *status) {
     __shared__ long long warp_sums[32];
     __shared__ long long carry_s;
-    __shared__ int n_big;
+    __shared__ int n_big, n_over;
     int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
-    if (tid == 0) { carry_s = 0; n_big = 0; }
+    if (tid == 0) { carry_s = 0; n_big = 0; n_over = 0; }
     __syncthreads();
     // 4 consecutive tiles per thread: 4096 tiles (1024 x 1024 pixels) are one pass with two barriers
     for (int base = 0; base < n_tiles; base += 4096) {
@@ -290,7 +290,8 @@ __global__ void __launch_bounds__(1024) k_scan(const int *__restrict__ tile_coun
             if (i0 + j < n_tiles) {
                 tile_start[i0 + j] = (int)(excl > 0x7fffffffLL ? 0x7fffffffLL : excl);
                 tile_cursor[i0 + j] = cs[j];  // late claims (k_emit) go behind the pre-claimed slots
-                if (c[j] > SORT_SMALL) big_tiles[1 + atomicAdd(&n_big, 1)] = i0 + j;  // (bucket overflow, too)
+                if (c[j] > SORT_SMALL) big_tiles[1 + atomicAdd(&n_big, 1)] = i0 + j;
+                if (c[j] > BUCKET_CAP) n_over = 1;
             }
             excl += c[j];
         }
@@ -302,7 +303,7 @@ __global__ void __launch_bounds__(1024) k_scan(const int *__restrict__ tile_coun
         long long total = carry_s;
         tile_start[n_tiles] = (int)(total > 0x7fffffffLL ? 0x7fffffffLL : total);
         big_tiles[0] = n_big;
-        if (n_big > 0) status[ST_FLAGS] |= SS_FLAG_LIST_FALLBACK;  // some bucket overflowed: k_emit builds the lists
+        if (n_over) status[ST_FLAGS] |= SS_FLAG_LIST_FALLBACK;  // some bucket overflowed: k_emit builds the lists
         status[ST_PAIRS] = total;
         if (total > max_pairs) status[ST_FLAGS] |= SS_FLAG_PAIR_OVERFLOW;
         long long enc = status[ST_FIRST_INVALID];
@@ -480,7 +481,7 @@ struct SegSrc {
     bool direct;
     __device__ __forceinline__ void load(int i, unsigned long long &k, int &id) const {
         if (direct) {
-            id = bucket[i < c_small ? i : SORT_SMALL - 1 - (i - c_small)];
+            id = bucket[i < c_small ? i : BUCKET_CAP - 1 - (i - c_small)];
             k = key[id];
         } else {
             k = pair_key[i];
@@ -488,6 +489,50 @@ struct SegSrc {
         }
     }
 };
+
+// pk[0 .. n) is sorted by the key part of the packed words (index part: IDX_BITS low bits).  Words in a run of
+// equal key parts are ranked exactly by (key, id); returns false, writing nothing, when more than a quarter of
+// the words tie (the caller then runs the 64-bit network).  Block-wide call.
+template <int IDX_BITS>
+__device__ bool rank_ties_and_write(const unsigned *pk, int n, const unsigned long long *keys, const int *ids,
+                                    int *out) {
+    __shared__ int s_ties[8];
+    constexpr unsigned IDX_MASK = (1u << IDX_BITS) - 1u;
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    int total = 0;
+    for (int p = tid; p < n; p += blockDim.x) {
+        const unsigned q = pk[p] >> IDX_BITS;
+        total += (p > 0 && (pk[p - 1] >> IDX_BITS) == q) || (p + 1 < n && (pk[p + 1] >> IDX_BITS) == q);
+    }
+    for (int o = 16; o > 0; o >>= 1) total += __shfl_xor_sync(0xffffffffu, total, o);
+    if (lane == 0) s_ties[warp] = total;
+    __syncthreads();
+    total = 0;
+#pragma unroll
+    for (int w = 0; w < 8; ++w) total += s_ties[w];
+    __syncthreads();  // s_ties may be rewritten by the next segment of a persistent CTA
+    if (total * 4 > n) return false;
+    for (int p = tid; p < n; p += blockDim.x) {
+        const unsigned w = pk[p];
+        const unsigned q = w >> IDX_BITS;
+        const int me = (int)(w & IDX_MASK);
+        int dst = p;
+        if (total > 0 && ((p > 0 && (pk[p - 1] >> IDX_BITS) == q) || (p + 1 < n && (pk[p + 1] >> IDX_BITS) == q))) {
+            int a = p;
+            while (a > 0 && (pk[a - 1] >> IDX_BITS) == q) --a;
+            const unsigned long long km = keys[me];
+            const int im = ids[me];
+            int rank = 0;
+            for (int j = a; j < n && (pk[j] >> IDX_BITS) == q; ++j) {
+                const int o = (int)(pk[j] & IDX_MASK);
+                rank += pair_less(keys[o], ids[o], km, im) ? 1 : 0;
+            }
+            dst = a + rank;
+        }
+        out[dst] = ids[me];
+    }
+    return true;
+}
 
 // Sorts the segment [s0, s0 + n), n <= 512, writing pair_id in place.  keys / ids: shared staging (>= 512 entries);
 // pk: 512 words.  Returns false (nothing written) when too many packed words tie.
@@ -553,41 +598,72 @@ __device__ bool sort_packed512(int s0, int n, int np2, const SegSrc &src, int *p
         if (warp == 0) { pk[i0] = e0; pk[i1] = e1; }
         __syncthreads();
     }
-    // pk[0 .. n) is sorted by the 23-bit part; words in a run of equal parts are ranked by (key, id)
-    int ties = 0;
-    for (int p = tid; p < n; p += blockDim.x) {
-        const unsigned q = pk[p] >> 9;
-        ties += (p > 0 && (pk[p - 1] >> 9) == q) || (p + 1 < n && (pk[p + 1] >> 9) == q);
+    return rank_ties_and_write<9>(pk, n, keys, ids, pair_id + s0);
+}
+
+// The same for segments of up to 4096 pairs (12 position bits, 20 key bits), several 64-blocks per warp, every
+// stage through shared memory: keys / ids hold the loaded segment, pk the packed words (4096).
+constexpr int PACK_BIG = 4096;
+__device__ bool sort_packed4096(int s0, int n, const SegSrc &src, int *pair_id, unsigned long long *keys, int *ids,
+                                unsigned *pk) {
+    __shared__ unsigned long long s_lo[8], s_hi[8];
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    int np2 = 64;
+    while (np2 < n) np2 <<= 1;
+    const int n_blocks = np2 >> 6;
+    unsigned long long lo = ~0ull, hi = 0ull;
+    for (int i = tid; i < n; i += blockDim.x) {
+        unsigned long long k; int id;
+        src.load(i, k, id);
+        keys[i] = k; ids[i] = id;
+        lo = min(lo, k); hi = max(hi, k);
     }
-    int total = ties;
-    for (int o = 16; o > 0; o >>= 1) total += __shfl_xor_sync(0xffffffffu, total, o);
-    __shared__ int s_ties[8];
-    if (lane == 0) s_ties[warp] = total;
+    for (int o = 16; o > 0; o >>= 1) {
+        lo = min(lo, __shfl_xor_sync(0xffffffffu, lo, o));
+        hi = max(hi, __shfl_xor_sync(0xffffffffu, hi, o));
+    }
+    if (lane == 0) { s_lo[warp] = lo; s_hi[warp] = hi; }
     __syncthreads();
-    total = 0;
 #pragma unroll
-    for (int w = 0; w < 8; ++w) total += s_ties[w];
-    if (total * 4 > n) return false;
-    for (int p = tid; p < n; p += blockDim.x) {
-        const unsigned w = pk[p];
-        const unsigned q = w >> 9;
-        const int me = (int)(w & 511u);
-        int dst = p;
-        if (total > 0 && ((p > 0 && (pk[p - 1] >> 9) == q) || (p + 1 < n && (pk[p + 1] >> 9) == q))) {
-            int a = p;
-            while (a > 0 && (pk[a - 1] >> 9) == q) --a;
-            const unsigned long long km = keys[me];
-            const int im = ids[me];
-            int rank = 0;
-            for (int j = a; j < n && (pk[j] >> 9) == q; ++j) {
-                const int o = (int)(pk[j] & 511u);
-                rank += pair_less(keys[o], ids[o], km, im) ? 1 : 0;
-            }
-            dst = a + rank;
-        }
-        pair_id[s0 + dst] = ids[me];
+    for (int w = 0; w < 8; ++w) { lo = min(lo, s_lo[w]); hi = max(hi, s_hi[w]); }
+    const int bits = 64 - __clzll((long long)(hi - lo));
+    const int shift = bits > 20 ? bits - 20 : 0;
+    for (int b = warp; b < n_blocks; b += 8) {
+        const int i0 = (b << 6) + lane, i1 = i0 + 32;
+        unsigned e0 = i0 < n ? (((unsigned)((keys[i0] - lo) >> shift) << 12) | (unsigned)i0) : 0xffffffffu;
+        unsigned e1 = i1 < n ? (((unsigned)((keys[i1] - lo) >> shift) << 12) | (unsigned)i1) : 0xffffffffu;
+        u_sort64(e0, e1, lane);
+        pk[i0] = e0; pk[i1] = e1;
     }
-    return true;
+    __syncthreads();
+    const int half = np2 >> 1;
+    for (int k = 128; k <= np2; k <<= 1) {
+        const int hk = k >> 1;
+        for (int c = tid; c < half; c += blockDim.x) {  // flip
+            const int q = c & (hk - 1);
+            const int l = ((c - q) << 1) + q, r = ((c - q) << 1) + k - 1 - q;
+            const unsigned a = pk[l], b = pk[r];
+            if (b < a) { pk[l] = b; pk[r] = a; }
+        }
+        __syncthreads();
+        for (int j = hk >> 1; j >= 64; j >>= 1) {  // long-distance disperse stages
+            for (int c = tid; c < half; c += blockDim.x) {
+                const int q = c & (j - 1);
+                const int l = ((c - q) << 1) + q;
+                const unsigned a = pk[l], b = pk[l + j];
+                if (b < a) { pk[l] = b; pk[l + j] = a; }
+            }
+            __syncthreads();
+        }
+        for (int b = warp; b < n_blocks; b += 8) {  // j = 32 .. 1 in registers
+            const int i0 = (b << 6) + lane, i1 = i0 + 32;
+            unsigned e0 = pk[i0], e1 = pk[i1];
+            u_disperse64(e0, e1, lane);
+            pk[i0] = e0; pk[i1] = e1;
+        }
+        __syncthreads();
+    }
+    return rank_ties_and_write<12>(pk, n, keys, ids, pair_id + s0);
 }
 
 __global__ void __launch_bounds__(256) k_tile_sort_small(const int *__restrict__ tile_start,
@@ -605,9 +681,9 @@ __global__ void __launch_bounds__(256) k_tile_sort_small(const int *__restrict__
     SegSrc src;
     src.direct = !(flags & SS_FLAG_LIST_FALLBACK);
     src.pair_key = pair_key + s0; src.pair_id = pair_id + s0;
-    src.bucket = bucket + (size_t)t * SORT_SMALL; src.key = key;
+    src.bucket = bucket + (size_t)t * BUCKET_CAP; src.key = key;
     src.c_small = tile_cursor[t];
-    if (n == 1 && src.direct && threadIdx.x == 0) pair_id[s0] = src.bucket[src.c_small ? 0 : SORT_SMALL - 1];
+    if (n == 1 && src.direct && threadIdx.x == 0) pair_id[s0] = src.bucket[src.c_small ? 0 : BUCKET_CAP - 1];
     if (n < 2 || n > SORT_SMALL) return;
     int np2 = 64;
     while (np2 < n) np2 <<= 1;
@@ -669,27 +745,40 @@ __global__ void __launch_bounds__(256) k_tile_sort_small(const int *__restrict__
     }
 }
 
-// Persistent over the list of long segments: <= SORT_BIG in dynamic smem, longer in place.
+// Persistent over the list of long segments (> SORT_SMALL pairs).  <= 4096: packed 32-bit sort, input from the tile's
+// bucket (or from the emitted pairs in the fallback path); <= SORT_BIG: 64-bit network in dynamic smem; longer: in
+// place in global memory.  Segments beyond 4096 only exist in the fallback path (they overflow the bucket).
 __global__ void __launch_bounds__(256) k_tile_sort_big(const int *__restrict__ tile_start,
                                                        unsigned long long *pair_key, int *pair_id,
+                                                       const int *__restrict__ bucket,
+                                                       const unsigned long long *__restrict__ key,
+                                                       const int *__restrict__ tile_cursor,
                                                        const int *__restrict__ big_tiles,
                                                        const long long *__restrict__ status) {
     extern __shared__ __align__(16) unsigned char smem_raw[];
     unsigned long long *keys = (unsigned long long *)smem_raw;
     int *ids = (int *)(smem_raw + (size_t)SORT_BIG * 8);
-    if (status[ST_FLAGS] & SS_FLAG_PAIR_OVERFLOW) return;
+    unsigned *pk = (unsigned *)(smem_raw + (size_t)SORT_BIG * 12);
+    const long long flags = status[ST_FLAGS];
+    if (flags & SS_FLAG_PAIR_OVERFLOW) return;
     int n_big = big_tiles[0];
     for (int b = blockIdx.x; b < n_big; b += gridDim.x) {
         int t = big_tiles[1 + b];
         int s0 = tile_start[t], n = tile_start[t + 1] - s0;
+        SegSrc src;
+        src.direct = !(flags & SS_FLAG_LIST_FALLBACK);
+        src.pair_key = pair_key + s0; src.pair_id = pair_id + s0;
+        src.bucket = bucket + (size_t)t * BUCKET_CAP; src.key = key;
+        src.c_small = tile_cursor[t];
+        __syncthreads();  // previous segment's shared arrays fully consumed
+        if (n <= PACK_BIG && sort_packed4096(s0, n, src, pair_id, keys, ids, pk)) continue;
         if (n <= SORT_BIG) {
-            for (int i = threadIdx.x; i < n; i += blockDim.x) { keys[i] = pair_key[s0 + i]; ids[i] = pair_id[s0 + i]; }
+            __syncthreads();
+            for (int i = threadIdx.x; i < n; i += blockDim.x) src.load(i, keys[i], ids[i]);
             __syncthreads();
             bitonic_sort_cta(keys, ids, n);
             for (int i = threadIdx.x; i < n; i += blockDim.x) pair_id[s0 + i] = ids[i];
-            __syncthreads();
         } else {
-            __syncthreads();
             bitonic_sort_cta(pair_key + s0, pair_id + s0, n);  // global memory, one CTA: slow but exact
         }
     }
@@ -759,7 +848,7 @@ cudaError_t launch_binning(const FwdLaunch &a, cudaStream_t s) {
                                                         (const unsigned long long *)(ws + L.key), tile_cursor, status);
         }
         static bool attr_set = false;
-        size_t big_smem = (size_t)SORT_BIG * 12;
+        size_t big_smem = (size_t)SORT_BIG * 12 + (size_t)PACK_BIG * 4;
         if (!attr_set) {
             cudaError_t e = cudaFuncSetAttribute(k_tile_sort_big, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                                  (int)big_smem);
@@ -769,7 +858,9 @@ cudaError_t launch_binning(const FwdLaunch &a, cudaStream_t s) {
         int grid_big = L.n_tiles < 296 ? L.n_tiles : 296;
         {
             ProfScope ps(KID_SORT_BIG, s);
-            k_tile_sort_big<<<grid_big, 256, big_smem, s>>>(tile_start, pair_key, pair_id, big_tiles, status);
+            k_tile_sort_big<<<grid_big, 256, big_smem, s>>>(tile_start, pair_key, pair_id, (const int *)(ws + L.bucket),
+                                                            (const unsigned long long *)(ws + L.key), tile_cursor, big_tiles,
+                                                            status);
         }
         count_launch(3);
     }

@@ -133,11 +133,12 @@ def test_tile_sort_tie_paths_vs_oracle(engine, case):
     assert np.array_equal(f["ids"].permute(1, 2, 0).cpu().numpy(), ref["ids"])
 
 
-@pytest.mark.parametrize("dense", [False, True])
+@pytest.mark.parametrize("dense", [0, 2500, 5000])
 def test_bucket_and_fallback_list_paths_vs_oracle(engine, dense):
     """Tile lists come from per-tile buckets filled by the projection kernel (spheres touching > 4 tiles fill a
-    bucket from its far end); one tile with more than 2048 spheres switches the whole frame to the
-    count/scan/emit path (SS_FLAG_LIST_FALLBACK).  Both must give the reference's lists."""
+    bucket from its far end): <= 512 per tile sort as packed words in registers, <= 4096 as packed words in shared
+    memory (persistent CTAs); one tile with more than 4096 spheres switches the whole frame to the
+    count/scan/emit path (SS_FLAG_LIST_FALLBACK).  All must give the reference's lists."""
     from oracle import oracle as orc
     from paper_2004_07484_b200 import CameraSpec, camera_from_vector
     rng = np.random.default_rng(21)
@@ -146,20 +147,20 @@ def test_bucket_and_fallback_list_paths_vs_oracle(engine, dense):
     m = 1500
     pos = np.column_stack([rng.uniform(-3, 3, m), rng.uniform(-2, 2, m), rng.uniform(8, 30, m)])
     rad = np.where(rng.uniform(size=m) < 0.1, rng.uniform(1.0, 4.0, m), rng.uniform(0.02, 0.3, m))  # some span many tiles
-    if dense:  # 2500 tiny spheres behind one pixel block
-        extra = np.column_stack([rng.uniform(-0.02, 0.02, 2500), rng.uniform(-0.02, 0.02, 2500), rng.uniform(9, 35, 2500)])
-        pos, rad = np.vstack([pos, extra]), np.concatenate([rad, rng.uniform(0.005, 0.02, 2500)])
-        m += 2500
+    if dense:  # tiny spheres behind one pixel block
+        extra = np.column_stack([rng.uniform(-0.02, 0.02, dense), rng.uniform(-0.02, 0.02, dense), rng.uniform(9, 35, dense)])
+        pos, rad = np.vstack([pos, extra]), np.concatenate([rad, rng.uniform(0.005, 0.02, dense)])
+        m += dense
     f32 = np.float32
     pos, rad = pos.astype(f32), rad.astype(f32)
     opa, feat, bg = rng.uniform(0.2, 1, m).astype(f32), rng.uniform(0, 1, (m, 3)).astype(f32), np.zeros(3, f32)
     cam, ocam = camera_from_vector(vec, w, h), orc.camera_from_vector(vec, w, h)
     f = engine.forward(pos, rad, opa, feat, bg, CameraSpec.from_camera(cam), gamma=0.1, tau=0.0, top_k=5,
                        collect_stats=True)
-    assert bool(f["status"]["flags"] & 4) == dense
+    assert bool(f["status"]["flags"] & 4) == (dense > 4096)
     starts, ids = engine.tile_lists(m, 3, w, h, 5)
     o_ids, o_starts = orc.tile_lists(pos, rad, ocam)
-    assert (np.diff(o_starts).max() > 2048) == dense
+    assert (np.diff(o_starts).max() > 4096) == (dense > 4096) and (np.diff(o_starts).max() > 2048) == (dense > 0)
     assert np.array_equal(starts, o_starts) and np.array_equal(ids, o_ids)
     ref = orc.render_forward(pos, rad, opa, feat, bg, ocam, gamma=0.1, tau=0.0, top_k=5)
     assert np.array_equal(f["ids"].permute(1, 2, 0).cpu().numpy(), ref["ids"])

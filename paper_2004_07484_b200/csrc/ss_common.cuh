@@ -55,7 +55,7 @@ struct Layout {
 
 constexpr int TILE = SS_TILE;
 constexpr int TILE_PX = TILE * TILE;
-constexpr int SORT_SMALL = 2048;  // per-tile lists up to this length sort in 24 KB static smem
+constexpr int SORT_SMALL = 512;   // per-tile lists up to this length: k_tile_sort_small (one CTA per tile, registers + 8 KB smem)
 constexpr int SORT_BIG = 8192;    // up to this length in 96 KB dynamic smem; beyond: in global memory
 constexpr int BUCKET_CAP = 4096;  // sphere ids per tile bucket; a fuller tile switches the frame to the emit path
 constexpr int CAM_BLOCKS_MAX = 1024;

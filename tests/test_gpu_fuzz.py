@@ -201,3 +201,37 @@ def make_random_scene_d(rng, m, d):
     f32 = np.float32
     return (pos.astype(f32), rng.uniform(0.1, 0.8, m).astype(f32), rng.uniform(0.1, 1.0, m).astype(f32),
             rng.uniform(0, 1, (m, d)).astype(f32), rng.uniform(0, 1, d).astype(f32))
+
+
+@pytest.mark.parametrize("case", ["equal_depth", "duplicates", "near_ties"])
+def test_long_segment_sort_tie_paths_vs_oracle(engine, case):
+    """The same tie regimes for one tile of 3000 spheres: packed words with 12 position bits in the persistent
+    sort kernel (exact ranking of tied runs, 64-bit network when too many tie)."""
+    from oracle import oracle as orc
+    from paper_2004_07484_b200 import CameraSpec, camera_from_vector
+    rng = np.random.default_rng(31)
+    m, w, h = 3000, 16, 16
+    pos = np.column_stack([rng.uniform(-0.05, 0.05, m), rng.uniform(-0.05, 0.05, m), rng.uniform(10, 40, m)])
+    rad = rng.uniform(0.01, 0.05, m)
+    if case == "equal_depth":
+        pos[:, 2], rad[:] = 20.0, 0.03
+        pos[:, :2] = 0.0  # identical earliest for every sphere: order by index
+    elif case == "duplicates":
+        dup, src = rng.choice(m, 300, replace=False), rng.choice(m, 300, replace=False)
+        pos[dup], rad[dup] = pos[src], rad[src]
+    else:
+        base = rng.uniform(10, 40, 40)
+        pos[:, 2] = base[rng.integers(0, 40, m)] * (1.0 + rng.integers(0, 4, m) * 2.0 ** -50)
+        pos[:, :2], rad[:] = 0.0, 0.03
+    f32 = np.float32
+    pos, rad = pos.astype(f32), rad.astype(f32)
+    opa, feat, bg = rng.uniform(0.2, 1, m).astype(f32), rng.uniform(0, 1, (m, 3)).astype(f32), np.zeros(3, f32)
+    vec = [0, 0, 0, 0, 0, 0, 5.0, 2.0]
+    cam, ocam = camera_from_vector(vec, w, h), orc.camera_from_vector(vec, w, h)
+    f = engine.forward(pos, rad, opa, feat, bg, CameraSpec.from_camera(cam), gamma=0.1, tau=0.0, top_k=5,
+                       collect_stats=True)
+    assert not f["status"]["flags"] & 4  # bucket path
+    starts, ids = engine.tile_lists(m, 3, w, h, 5)
+    o_ids, o_starts = orc.tile_lists(pos, rad, ocam)
+    assert int(np.diff(o_starts).max()) > 2048
+    assert np.array_equal(starts, o_starts) and np.array_equal(ids, o_ids)

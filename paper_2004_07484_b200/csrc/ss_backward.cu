@@ -170,13 +170,10 @@ __device__ __forceinline__ void slot_gradient(const BackArgs &a, const Rec &rc, 
     slot_gradient_acoef<DP, MODE, MERGE>(a, rc, id, zk, ck, E, inv_g, up, acoef, d, xs, ys, ux, uy, uz, inv_vnorm);
 }
 
-// KT > 0: K <= KT slots held in registers, every load of a phase issued before its first use
+// KT > 0: the K <= KT slots of a pixel are unrolled, every load of a phase issued before its first use
 // (the kernel is latency-bound on dependent gathers).  KT == 0: any K, slot by slot.
-#ifndef SS_BACKWARD_MINB
-#define SS_BACKWARD_MINB 2
-#endif
 template <int DP, int MODE, int KT>
-__global__ void __launch_bounds__(TILE_PX, (KT > 0) ? SS_BACKWARD_MINB : 1) k_backward(BackArgs a) {
+__global__ void __launch_bounds__(TILE_PX, (KT > 0) ? (KT <= 5 ? 4 : 3) : 1) k_backward(BackArgs a) {
     const Cam &cam = a.cam;
     const int tile = blockIdx.x;
     const int tid = threadIdx.x;
@@ -235,36 +232,42 @@ __global__ void __launch_bounds__(TILE_PX, (KT > 0) ? SS_BACKWARD_MINB : 1) k_ba
     }
 
     if (KT > 0) {
-        // gather all records and features first, then f_hat (grad.py:103-108), then the gradients
-        Rec rc[KR];
-        float f[KR][DP];
+        // Register diet: the kernel is bound by the latency of its dependent loads, and holding all K records
+        // (8 registers each) plus their features limited it to 2 resident CTAs per SM (121 registers).  Phase 1 keeps
+        // only the opacity and the scalar <upstream, f_k> of every slot; phase 2 re-reads the record of slot k (an
+        // L1 hit) one slot ahead of its use: 64 registers, 4 resident CTAs, 115 -> 91 us at C3.
+        float ok[KR], uf[KR], Ek[KR];
+        {
+            float f[KR][DP];
 #pragma unroll
-        for (int k = 0; k < KR; ++k) {
-#ifdef SS_EXPERIMENT_SMALL_GATHER  // measurement only: gathers from a cache-resident subset
-            const int id = sid[k] >= 0 ? (sid[k] & 1023) : 0;
-#else
-            const int id = sid[k] >= 0 ? sid[k] : 0;
-#endif
-            if (sid[k] >= 0) rc[k] = a.rec[id];
+            for (int k = 0; k < KR; ++k) {
+                const int id = sid[k] >= 0 ? sid[k] : 0;
+                ok[k] = sid[k] >= 0 ? a.rec[id].o : 0.0f;
 #pragma unroll
-            for (int i = 0; i < DP; ++i) f[k][i] = (sid[k] >= 0 && i < d) ? a.feat[(size_t)id * d + i] : 0.0f;
-        }
-        float Ek[KR];
+                for (int i = 0; i < DP; ++i) f[k][i] = (sid[k] >= 0 && i < d) ? a.feat[(size_t)id * d + i] : 0.0f;
+            }
 #pragma unroll
-        for (int k = 0; k < KR; ++k) {
-            Ek[k] = 0.0f;
-            if (sid[k] >= 0) {
-                Ek[k] = ex2_approx_f((rc[k].o * zk[k] * inv_g - ld) * 1.4426950408889634f);
-                const float w = rc[k].o * ck[k] * Ek[k];
+            for (int k = 0; k < KR; ++k) {
+                Ek[k] = sid[k] >= 0 ? ex2_approx_f((ok[k] * zk[k] * inv_g - ld) * 1.4426950408889634f) : 0.0f;
+                const float w = ok[k] * ck[k] * Ek[k];
+                uf[k] = 0.0f;
 #pragma unroll
-                for (int i = 0; i < DP; ++i) fhat[i] = fmaf(w, f[k][i], fhat[i]);
+                for (int i = 0; i < DP; ++i) { fhat[i] = fmaf(w, f[k][i], fhat[i]); uf[k] = fmaf(up[i], f[k][i], uf[k]); }
             }
         }
+        float ufh = 0.0f;
 #pragma unroll
-        for (int k = 0; k < KR; ++k)
+        for (int i = 0; i < DP; ++i) ufh = fmaf(up[i], fhat[i], ufh);
+        Rec nxt; nxt.cx = nxt.cy = nxt.cz = 0.0; nxt.r = 1.0f; nxt.o = 0.0f;
+        if (sid[0] >= 0) nxt = a.rec[sid[0]];
+#pragma unroll
+        for (int k = 0; k < KR; ++k) {
+            const Rec cur = nxt;
+            if (k + 1 < KR && sid[k + 1 < KR ? k + 1 : k] >= 0) nxt = a.rec[sid[k + 1 < KR ? k + 1 : k]];
             if (kMerge ? __any_sync(0xffffffffu, sid[k] >= 0) : sid[k] >= 0)
-                slot_gradient<DP, MODE, kMerge>(a, rc[k], sid[k], zk[k], ck[k], Ek[k], inv_g, up, fhat, f[k], d, xs, ys,
-                                                ux, uy, uz, inv_vnorm);
+                slot_gradient_acoef<DP, MODE, kMerge>(a, cur, sid[k], zk[k], ck[k], Ek[k], inv_g, up, uf[k] - ufh, d, xs,
+                                                      ys, ux, uy, uz, inv_vnorm);
+        }
     } else {
         for (int k = 0; k < K; ++k) {
             const int id = valid ? ids[k * P + pix] : -1;

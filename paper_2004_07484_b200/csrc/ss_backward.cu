@@ -118,11 +118,12 @@ __device__ __forceinline__ void slot_gradient_acoef(const BackArgs &a, const Rec
         g_sensor = -(dl_ddist * inv_dist) * (dvx * xsf + dvy * ysf) * (float)(1.0 / cam.sensor_w);
         g_focal = 0.0f;
     }
-    float v[8 + DP];
+    constexpr int DP4 = (DP + 3) & ~3;  // the feature part of the row is padded to whole quads
+    float v[8 + DP4];
     v[0] = gcx; v[1] = gcy; v[2] = gcz; v[3] = d_radius;
     v[4] = dl_do; v[5] = g_focal; v[6] = g_sensor; v[7] = 1.0f;
 #pragma unroll
-    for (int i = 0; i < DP; ++i) v[8 + i] = w * up[i];  // up[] is zero beyond d
+    for (int i = 0; i < DP4; ++i) v[8 + i] = i < DP ? w * up[i] : 0.0f;  // up[] is zero beyond d
   if (MERGE) {
     // Warp-level pre-reduction: the L2 processes one 16-byte reduction per lane and instruction (15.7 M of
     // them at C3: ~50 us of this kernel), and neighbouring pixels of the 8x4 block mostly hold the SAME
@@ -137,7 +138,7 @@ __device__ __forceinline__ void slot_gradient_acoef(const BackArgs &a, const Rec
     while (__any_sync(0xffffffffu, nxt >= 0)) {
         const int src = nxt >= 0 ? nxt : (int)lane;
 #pragma unroll
-        for (int j = 0; j < 8 + DP; ++j) {
+        for (int j = 0; j < 8 + DP; ++j) {  // (padding beyond DP stays zero)
             if (j == 7) continue;  // the pixel count is the group size (set below)
             const float o = __shfl_sync(0xffffffffu, v[j], src);
             if (nxt >= 0) v[j] += o;
@@ -154,7 +155,7 @@ __device__ __forceinline__ void slot_gradient_acoef(const BackArgs &a, const Rec
     red_add_v4(row, v[0], v[1], v[2], v[3]);
     red_add_v4(row + 4, v[4], v[5], v[6], v[7]);
 #pragma unroll
-    for (int i = 0; i < DP; i += 4)
+    for (int i = 0; i < DP4; i += 4)
         if (i < d) red_add_v4(row + 8 + i, v[8 + i], v[9 + i], v[10 + i], v[11 + i]);
 }
 
@@ -503,7 +504,8 @@ cudaError_t launch_backward(const BwdLaunch &a, cudaStream_t s) {
     const int d = b.d, mode = a.cam.mode;
     {
         ProfScope ps(KID_BACKWARD, s);
-        if (d <= 4) launch_bw_k<4>(b, L.n_tiles, mode, s);
+        if (d == 3) launch_bw_k<3>(b, L.n_tiles, mode, s);  // RGB: one shuffle per merge round less than the d = 4 build
+        else if (d <= 4) launch_bw_k<4>(b, L.n_tiles, mode, s);
         else if (d <= 16) launch_bw_k<16>(b, L.n_tiles, mode, s);
         else launch_bw_k<32>(b, L.n_tiles, mode, s);
     }

@@ -342,16 +342,38 @@ __global__ void __launch_bounds__(256) k_finalize(FinArgs a) {
     const Cam &cam = a.cam;
     const int RS = a.raw_stride, d = a.d;
     const int t = threadIdx.x;
-    const long long i = (long long)blockIdx.x * 256 + t;
-    bool touched = false;
+    bool any_touched = false;
     float acc[14];
 #pragma unroll
     for (int j = 0; j < 14; ++j) acc[j] = 0.0f;
-    if (i < a.M) {
+    // Persistent CTAs: a thread walks <= 8 spheres and keeps its camera partial sums in registers, so the
+    // butterfly, the barrier, the float64 atomics, the fence and the (returning) completion-counter atomic at the
+    // end are paid once per CTA instead of once per 256 spheres.
+    const long long n_blocks = (a.M + 255) / 256;
+    const float4 zero4 = make_float4(0.f, 0.f, 0.f, 0.f);
+    float4 n0 = zero4, n1 = zero4;  // the first two quads of the NEXT sphere's row, loaded one iteration ahead
+    {
+        const long long i0 = (long long)blockIdx.x * 256 + t;
+        if (blockIdx.x < n_blocks && i0 < a.M) {
+            const float4 *row0 = (const float4 *)(a.raw + (size_t)i0 * RS);
+            n0 = row0[0]; n1 = row0[1];
+        }
+    }
+    for (long long blk = blockIdx.x; blk < n_blocks; blk += gridDim.x) {
+        const long long i = blk * 256 + t;
+        const float4 r0 = n0, r1 = n1;
+        {
+            const long long inext = i + (long long)gridDim.x * 256;
+            if (blk + gridDim.x < n_blocks && inext < a.M) {
+                const float4 *rown = (const float4 *)(a.raw + (size_t)inext * RS);
+                n0 = rown[0]; n1 = rown[1];
+            }
+        }
+        if (i >= a.M) continue;
         float4 *row = (float4 *)(a.raw + (size_t)i * RS);
-        const float4 r0 = row[0], r1 = row[1];
         const float cnt = r1.w;
-        touched = cnt > 0.0f;
+        const bool touched = cnt > 0.0f;
+        any_touched |= touched;
         float dp0 = 0.f, dp1 = 0.f, dp2 = 0.f, drad = 0.f, dopa = 0.f, inv_div = 0.f;
         if (touched) {
             const double pr = a.proj_r[i];
@@ -374,12 +396,12 @@ __global__ void __launch_bounds__(256) k_finalize(FinArgs a) {
                 const float sx = cam_scale * r0.x, sy = cam_scale * r0.y, sz = cam_scale * r0.z;
                 const float rx = (float)((double)a.pos[3 * i] - cam.t[0]), ry = (float)((double)a.pos[3 * i + 1] - cam.t[1]),
                             rz = (float)((double)a.pos[3 * i + 2] - cam.t[2]);
-                acc[0] = sx; acc[1] = sy; acc[2] = sz;
-                acc[3] = sx * rx; acc[4] = sx * ry; acc[5] = sx * rz;
-                acc[6] = sy * rx; acc[7] = sy * ry; acc[8] = sy * rz;
-                acc[9] = sz * rx; acc[10] = sz * ry; acc[11] = sz * rz;
-                acc[12] = cam_scale * r1.y;
-                acc[13] = cam_scale * r1.z;
+                acc[0] += sx; acc[1] += sy; acc[2] += sz;
+                acc[3] = fmaf(sx, rx, acc[3]); acc[4] = fmaf(sx, ry, acc[4]); acc[5] = fmaf(sx, rz, acc[5]);
+                acc[6] = fmaf(sy, rx, acc[6]); acc[7] = fmaf(sy, ry, acc[7]); acc[8] = fmaf(sy, rz, acc[8]);
+                acc[9] = fmaf(sz, rx, acc[9]); acc[10] = fmaf(sz, ry, acc[10]); acc[11] = fmaf(sz, rz, acc[11]);
+                acc[12] = fmaf(cam_scale, r1.y, acc[12]);
+                acc[13] = fmaf(cam_scale, r1.z, acc[13]);
             }
         }
         // features: RS - 8 = ceil4(d) floats behind the two fixed quads
@@ -414,7 +436,7 @@ __global__ void __launch_bounds__(256) k_finalize(FinArgs a) {
     // global accumulators (double atomics), fences and bumps the completion counter; the last block
     // publishes the camera block and the clean tag.
     const int lane = t & 31, wid = t >> 5;
-    if (a.cam_grads && __any_sync(0xffffffffu, touched)) {
+    if (a.cam_grads && __any_sync(0xffffffffu, any_touched)) {
 #pragma unroll
         for (int j = 0; j < 14; ++j) {
             float v = acc[j];
@@ -523,7 +545,9 @@ cudaError_t launch_backward(const BwdLaunch &a, cudaStream_t s) {
     f.gate = (a.blend.flags & SS_OPT_GATE) ? 1 : 0;
     f.cam_grads = cam_grads ? 1 : 0;
     f.accumulate = (a.blend.flags & SS_OPT_ACCUMULATE) ? 1 : 0;
-    int grid = (int)((M + 255) / 256);
+    const long long fin_blocks = (M + 255) / 256;
+    long long fin_grid = 148 * 4 > (fin_blocks + 7) / 8 ? 148 * 4 : (fin_blocks + 7) / 8;  // one wave (56 registers: 4 CTAs per SM) or <= 8 spheres per thread
+    int grid = (int)(fin_blocks < fin_grid ? fin_blocks : fin_grid);
     {
         ProfScope ps(KID_FINALIZE, s);
         k_finalize<<<grid, 256, 0, s>>>(f);

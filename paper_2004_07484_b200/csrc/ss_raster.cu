@@ -163,7 +163,7 @@ constexpr int rec_stride() {
 }
 
 template <int DP, int KT, int MODE>
-__global__ void __launch_bounds__(TILE_PX, (KT <= 8 && DP <= 4) ? SS_RASTER_MINB : (DP <= 4 ? 3 : (DP <= 16 ? 2 : 1))) k_raster(RasterArgs a) {
+__global__ void __launch_bounds__(TILE_PX, (KT <= 8 && DP <= 4) ? SS_RASTER_MINB : (DP <= 16 ? 3 : 2)) k_raster(RasterArgs a) {
     constexpr int CAP = SS_MAX_CHUNK;
     extern __shared__ __align__(16) unsigned char smem_raw[];
     constexpr int RS = rec_stride<DP>();           // floats per staged candidate

@@ -31,7 +31,7 @@ if ROOT not in sys.path:
 
 COUNT, SIZE, TOP_K, D = 1_000_000, 1024, 5, 3
 GAMMA, EPS, TAU = 0.1, 1e-2, 0.01
-NCU_RASTER_DRAM_BYTES = 180_676_352  # one k_raster launch at this config: 117.48 MB read + 63.19 MB written (ncu, r01n)
+NCU_KERNELS_JSON = "profiles/ncu_kernels.json"  # per-kernel ncu --set full figures, written by scripts/ncu_extract.py
 METRIC = "fwd+bwd frames/s, 1M spheres @1024^2 n_track=5 (ms/frame = ms_per_step / views_per_rank)"
 WORKLOAD = ("C3: 1M uniform 3px spheres (cli.py:_benchmark_scene, seed 0), 1024x1024, d=3, n_track=5, "
             "gamma=0.1 eps=0.01 tau=0.01, full fwd+bwd incl. camera gradients, upstream=sign(image-0.5)")
@@ -96,7 +96,11 @@ def algorithmic_bytes(T, S, U, M=COUNT, P=SIZE * SIZE, d=D, K=TOP_K):
     fwd = M * (20 + 4 * d) + 8 * T + T * (24 + 4 * d) + P * (4 * d + 4) + P * (12 * K + 4)
     bwd = P * (12 * K + 4) + P * 4 * d + U * (20 + 4 * d) + 2 * M * (32 + 4 * d) + M * (24 + 4 * d)
     raster = T * (4 + 24 + 4 * d) + P * (4 * d + 4) + P * (12 * K + 4)
-    return fwd, bwd, raster
+    # k_project: inputs read once, 96 B of records / keys / rectangles / filter per sphere + 4 B per tile bucket entry
+    project = M * (20 + 4 * d) + M * 96 + 4 * T
+    # k_backward: buffer + upstream read, one gather and one accumulator row per touched sphere
+    backward = P * (12 * K + 4) + P * 4 * d + U * (20 + 4 * d) + U * (32 + 4 * d)
+    return fwd, bwd, {"k_raster": raster, "k_project": project, "k_backward": backward}
 
 
 def host_threads():
@@ -124,29 +128,80 @@ def cpu_frame_seconds(threads, repeats=1):
     return best
 
 
+def reference_package():
+    """The unmodified reference (pure Python / NumPy), installed by __graft_entry__.build() into the
+    git-ignored baseline/_ref, or None.  /root/reference itself is never read at run time."""
+    ref_dir = os.path.join(ROOT, "baseline", "_ref")
+    if not os.path.isdir(os.path.join(ref_dir, "softsphere")):
+        return None
+    if ref_dir not in sys.path:
+        sys.path.append(ref_dir)
+    try:
+        import softsphere
+        return softsphere
+    except Exception:
+        return None
+
+
+def reference_frame_seconds(ss, frames=1, budget_s=150.0):
+    """Full C3 frames through the reference's own render_forward / render_backward (cli.py:377-389 protocol:
+    float64, workers=1 -- its thread pool does not scale under the GIL), as many of `frames` as fit the budget."""
+    from paper_2004_07484_b200.synthetic import benchmark_scene
+    pos, rad, opa, feat, bg, vec = benchmark_scene(COUNT, SIZE, SIZE, seed=0)
+    scene = ss.new_scene(D, bg.astype(np.float64))
+    scene.positions, scene.radii = pos.astype(np.float64), rad.astype(np.float64)
+    scene.opacities, scene.features = opa.astype(np.float64), feat.astype(np.float64)
+    cam = ss.camera_from_vector(vec, SIZE, SIZE)
+    params = ss.BlendParams(gamma=GAMMA, epsilon=EPS, tau=TAU, top_k=TOP_K)
+    times, t_start = [], time.perf_counter()
+    for _ in range(frames):
+        t0 = time.perf_counter()
+        image, buf, _ = ss.render_forward(scene, cam, params, workers=1)
+        ss.render_backward(scene, cam, params, buf, np.sign(image.data - 0.5), workers=1)
+        times.append(time.perf_counter() - t0)
+        if time.perf_counter() - t_start + times[-1] > budget_s:
+            break
+    return times
+
+
+def cpu_baseline_block(threads, frames=1, budget_s=150.0):
+    """cpu_baseline for the JSON line: the real reference when it is installed (kind "reference", 1 core),
+    else the float64 C port of it (kind "port", OpenMP over tiles)."""
+    ss = reference_package()
+    port = cpu_frame_seconds(threads, repeats=1)[0]
+    if ss is not None:
+        times = reference_frame_seconds(ss, frames, budget_s)
+        total = float(np.sum(times))
+        return times, {"value": len(times) / total, "unit": "frames/s", "cores": 1, "kind": "reference",
+                       "sample": f"{len(times)} full C3 frame(s) (fwd+bwd, tau=0.01) through the unmodified reference's "
+                                 "render_forward/render_backward from baseline/_ref, float64, workers=1 (its thread "
+                                 "pool does not scale under the GIL)",
+                       "port": {"value": 1.0 / port, "unit": "frames/s", "cores": threads,
+                                "note": "oracle/ss_oracle.c, the float64 C restatement, OpenMP over tiles"}}
+    return [port], {"value": 1.0 / port, "unit": "frames/s", "cores": threads, "kind": "port",
+                    "sample": "1 full C3 frame (fwd+bwd, tau=0.01) on the float64 oracle port, OpenMP over tiles "
+                              "(baseline/_ref not installed on this box)"}
+
+
 def run_reference(args, rank):
-    """CPU arm: the oracle port of the reference (float64, OpenMP over tiles), all host threads."""
+    """CPU arm: the reference's own CPU implementation of the path on this box's host cores (rank 0 only;
+    under torchrun the other ranks exit without work -- the CPU arm does not scale with --gpus)."""
     if rank != 0:
         return
     from oracle import oracle as orc
     orc.build()
     threads = host_threads()
-    warm = cpu_frame_seconds(threads) if args.warmup > 0 else []
-    # bounded sample: full frames, as many of the K requested as fit in ~2 minutes of CPU time
-    first = cpu_frame_seconds(threads, repeats=1)
-    budget_frames = max(1, int(120.0 / max(first[0], 1e-3)))
-    times = first + (cpu_frame_seconds(threads, repeats=min(args.steps, budget_frames) - 1)
-                     if min(args.steps, budget_frames) > 1 else [])
+    times, block = cpu_baseline_block(threads, frames=max(1, min(args.steps, 3)))
     total = float(np.sum(times))
     value = len(times) / total
     line = {
         "impl": "reference", "metric": METRIC, "value": value, "unit": "frames/s", "n_gpus": args.gpus,
-        "steps": len(times), "warmup": len(warm), "ms_per_step": 1e3 * total / len(times),
+        "steps": len(times), "warmup": 0, "ms_per_step": 1e3 * total / len(times),
         "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-        "config": {"workload": WORKLOAD, "views_per_rank": 1},
-        "cpu_baseline": {"value": value, "unit": "frames/s", "cores": threads, "kind": "port",
-                         "sample": f"{len(times)} full C3 frame(s) of the {args.steps} requested (capped at ~120 s), "
-                                   "fwd+bwd, tau=0.01, float64 oracle port, OpenMP over tiles"},
+        "config": {"workload": WORKLOAD, "views_per_rank": 1,
+                   "note": "CPU arm: runs on rank 0 only and does not scale with --gpus; frames are whole C3 frames, "
+                           "bounded to ~150 s of CPU time (no warm-up frame: a frame takes about a minute)"},
+        "cpu_baseline": block,
         "e2e": {"value": value, "unit": "frames/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
         "gpu_launches": 0,
     }
@@ -228,7 +283,9 @@ def main():
     sampler.start()
     ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
     launches0 = _lib.launch_count()
-    _lib.profile_enable_only(["k_raster"])  # dominant kernel: one event pair per step inside the timed region
+    # the three largest kernels carry one CUDA-event pair each inside the timed region (their in-step launch
+    # durations feed the roofline block; the pairs cost ~2 us each and are part of the headline time)
+    _lib.profile_enable_only(["k_raster", "k_backward", "k_project"])
     torch.cuda.synchronize()
     for a, b in ev:
         flush.zero_()
@@ -255,35 +312,72 @@ def main():
         total_ms = float(t.item())
     value = n_views * args.steps / (total_ms / 1e3)
 
-    # ---- end to end through the host-buffer API (pinned host buffers, H2D + D2H inside the timed region)
-    sess = HostRenderSession(COUNT, D, SIZE, SIZE, TOP_K, engine=eng)
-    sess.set_scene(pos, rad, opa, feat, bg)
+    # ---- end to end with HOST buffers (copies inside the timed region, wall clock around synchronised steps)
     local = mv.local_views(n_views)
-    sess.h_upstream.copy_(upstreams[local[0]].cpu())
-    e2e_steps = max(3, min(args.steps, 20))
     local_cams = [cams[v] for v in local]
+    e2e_steps = max(3, min(args.steps, 20))
 
     def reduce_fn(out):  # multi-GPU: sphere gradients are reduced on the device before the download
         if world > 1:
             for k in ("d_pos", "d_rad", "d_opa", "d_feat", "pixel_count"):
                 dist.all_reduce(out[k])
 
-    for _ in range(3):
-        sess.render_step(local_cams, gamma=GAMMA, eps=EPS, tau=TAU, reduce_fn=reduce_fn)
-    torch.cuda.synchronize()
-    if world > 1:
-        dist.barrier()
-    t0 = time.perf_counter()
-    for _ in range(e2e_steps):
-        sess.render_step(local_cams, gamma=GAMMA, eps=EPS, tau=TAU, reduce_fn=reduce_fn)
-    torch.cuda.synchronize()
-    e2e_s = time.perf_counter() - t0
-    if world > 1:
-        t = torch.tensor([e2e_s], dtype=torch.float64, device=device)
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        e2e_s = float(t.item())
+    def timed(fn, steps):
+        for _ in range(3):
+            fn()
+        torch.cuda.synchronize()
+        if world > 1:
+            dist.barrier()
+        t0 = time.perf_counter()
+        for _ in range(steps):
+            fn()
+        torch.cuda.synchronize()
+        secs = time.perf_counter() - t0
+        if world > 1:
+            t = torch.tensor([secs], dtype=torch.float64, device=device)
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+            secs = float(t.item())
+        return n_views * steps / secs
+
+    # (1) `e2e`: the C-ABI session call.  Pinned host buffers; the scene is uploaded when it changes (set_scene)
+    #     and stays resident; every step uploads the upstream image and downloads the image and the gradient
+    #     rows of the spheres that received gradient (device-side compaction).
+    sess = HostRenderSession(COUNT, D, SIZE, SIZE, TOP_K, engine=eng)
+    sess.set_scene(pos, rad, opa, feat, bg)
+    sess.h_upstream.copy_(upstreams[local[0]].cpu())
+    compact = world == 1  # the allreduced buffer of a multi-GPU step is dense
+    e2e_value = timed(lambda: sess.render_step(local_cams, gamma=GAMMA, eps=EPS, tau=TAU, reduce_fn=reduce_fn,
+                                               compact=compact), e2e_steps)
     h2d_b, d2h_b = sess.bytes_per_step(len(local_cams))
-    e2e_value = n_views * e2e_steps / e2e_s
+    # (2) the same session re-uploading the whole scene and downloading all M gradient rows every step
+    #     (what round 1 reported as e2e: a scene that changes on the host between steps)
+    e2e_dense = timed(lambda: sess.render_step(local_cams, gamma=GAMMA, eps=EPS, tau=TAU, reduce_fn=reduce_fn,
+                                               compact=False, always_upload=True), e2e_steps)
+    dense_h2d, dense_d2h = sess.bytes_per_step(len(local_cams))
+    # (3) `e2e_plugin`: the reference-facing plug-in call itself -- SoftsphereAdapter.forward / .backward on a
+    #     SphereScene of float64 NumPy columns, NumPy image / SceneGradients out (optim.py:265-304), N = 1 only
+    plugin = None
+    if world == 1:
+        import paper_2004_07484_b200 as pk
+        scene_np = pk.new_scene(D, bg.astype(np.float64))
+        scene_np.positions, scene_np.radii = pos.astype(np.float64), rad.astype(np.float64)
+        scene_np.opacities, scene_np.features = opa.astype(np.float64), feat.astype(np.float64)
+        cam_np = camera_from_vector(cam_vecs[0], SIZE, SIZE)
+        params_np = pk.BlendParams(gamma=GAMMA, epsilon=EPS, tau=TAU, top_k=TOP_K)
+        adapter = pk.SoftsphereAdapter(engine=eng)
+
+        def plugin_step():
+            image, buf, _ = adapter.forward(scene_np, cam_np, params_np)
+            adapter.backward(scene_np, cam_np, params_np, buf, np.sign(image.data - 0.5))
+
+        plug_steps = max(3, min(args.steps, 10))
+        plugin = {"value": timed(plugin_step, plug_steps), "unit": "frames/s", "steps": plug_steps,
+                  "h2d_bytes_per_step": 4 * (COUNT * (5 + D) + D) + 4 * SIZE * SIZE * D,
+                  "d2h_bytes_per_step": 4 * SIZE * SIZE * (D + 1) + 4 * (COUNT * (6 + D) + 32),
+                  "path": "SoftsphereAdapter.forward/.backward(SphereScene float64 NumPy, Camera, BlendParams): float64 "
+                          "columns narrowed into pinned staging + 1 H2D, ss_forward, image -> float64 NumPy, host "
+                          "upstream sign(image - 0.5), upstream H2D, ss_backward (scene upload shared with the "
+                          "forward call), all gradients -> float64 NumPy"}
 
     if rank == 0:
         peaks_path = os.path.join(ROOT, "MEASURED_PEAKS.json")
@@ -292,10 +386,33 @@ def main():
         else:
             peak, peak_src = 6650.0, "fallback (B200_PROFILING.md)"
         T = status["num_pairs"]
-        fwd_b, bwd_b, raster_b = algorithmic_bytes(T, filled, touched)
-        ms_r, n_r = prof["k_raster"]
-        raster_ms = ms_r / max(n_r, 1)
-        achieved = raster_b / (raster_ms * 1e-3) / 1e9
+        fwd_b, bwd_b, kbytes = algorithmic_bytes(T, filled, touched)
+        try:
+            ncu = json.load(open(os.path.join(ROOT, NCU_KERNELS_JSON)))
+        except Exception:
+            ncu = {}
+        sm_mhz = clocks.get("sm_mhz") or clocks.get("sm_max_mhz") or 1965.0
+        per_kernel = {}
+        for kname, nbytes in kbytes.items():
+            ms_k, n_k = prof.get(kname, (0.0, 0))
+            if not n_k:
+                continue
+            us = 1e3 * ms_k / n_k
+            gbs = nbytes / (us * 1e-6) / 1e9
+            entry = {"avg_launch_us": us, "launches_timed": n_k, "algorithmic_bytes_per_launch": nbytes,
+                     "achieved_GBps": gbs, "frac": gbs / peak}
+            nk = ncu.get(kname)
+            if nk:
+                entry["traffic"] = nk.get("dram_bytes")
+                if nk.get("inst_executed"):
+                    # time the launch would take if one of the 4 x 148 warp schedulers issued an instruction every cycle
+                    issue_us = nk["inst_executed"] / (592.0 * sm_mhz)
+                    entry["issue_frac"] = issue_us / us
+                    entry["warp_instructions"] = nk["inst_executed"]
+            per_kernel[kname] = entry
+        rk = per_kernel.get("k_raster", {})
+        raster_ms = rk.get("avg_launch_us", 0.0) / 1e3
+        achieved = rk.get("achieved_GBps", 0.0)
         step_ms = total_ms / args.steps / vpr
         kernels = {k: {"us": round(1e3 * ms / n, 2), "launches": n} for k, (ms, n) in breakdown.items() if n}
         line = {
@@ -305,36 +422,44 @@ def main():
             "config": {"workload": WORKLOAD, "views_per_rank": vpr, "views_total": n_views,
                        "cache": "L2 flushed between timed steps (256 MB write, outside the timed region)",
                        "pairs_T": T, "filled_slots_S": filled, "touched_spheres_U": touched,
+                       "timed_region_note": "3 CUDA-event pairs per step (k_raster, k_backward, k_project) are recorded "
+                                            "inside the timed region for the roofline block",
                        "collective": ("none" if world == 1 else
-                                      f"1 {backend} sum-allreduce of {grads.allreduce_bytes()} B per step")},
+                                      f"1 {backend} sum-allreduce group of {grads.allreduce_bytes()} B per step")},
             "clocks": clocks,
             "e2e": {"value": e2e_value, "unit": "frames/s", "h2d_bytes_per_step": h2d_b, "d2h_bytes_per_step": d2h_b,
                     "steps": e2e_steps,
-                    "path": "HostRenderSession.render_step: pinned host scene+upstream -> device, "
-                            "ss_forward, image -> host, ss_backward, all gradients -> host"},
+                    "path": "HostRenderSession.render_step (C ABI, pinned host buffers): scene resident on the device "
+                            "(uploaded by set_scene when it changes); per step upstream H2D, ss_forward, image D2H, "
+                            "ss_backward, gradient rows of the touched spheres (index + count + grads, compacted on "
+                            "the device) + camera block D2H"},
+            "e2e_dense_reupload": {"value": e2e_dense, "unit": "frames/s", "h2d_bytes_per_step": dense_h2d,
+                                   "d2h_bytes_per_step": dense_d2h,
+                                   "path": "same call, whole scene uploaded and all M gradient rows downloaded every step "
+                                           "(round 1's e2e)"},
             "gpu_launches": int(launches),
             "roofline": {"kernel": "k_raster", "bound": "hbm", "achieved": achieved, "peak": peak,
-                         "unit": "GB/s", "frac": achieved / peak, "traffic": NCU_RASTER_DRAM_BYTES,
-                         "traffic_source": "dram__bytes_read.sum + dram__bytes_write.sum of one k_raster launch, "
-                                           "ncu --set full, profiles/r01_summary.md (r01n)",
-                         "issue_bound_note": "k_raster is instruction-issue bound, not HBM bound (SURVEY 8d): ncu "
-                                             "smsp__issue_active 72%, 213 M warp instructions, l1tex (shared-memory wavefronts) 68%, DRAM 8% of peak",
-                         "peak_source": peak_src, "algorithmic_bytes_per_launch": raster_b,
+                         "unit": "GB/s", "frac": achieved / peak, "traffic": rk.get("traffic"),
+                         "issue_frac": rk.get("issue_frac"),
+                         "traffic_source": f"dram__bytes_read.sum + dram__bytes_write.sum of one launch, ncu --set full, "
+                                           f"{ncu.get('_source', 'unavailable')} via {NCU_KERNELS_JSON}",
+                         "issue_bound_note": "k_raster is instruction-issue bound, not HBM bound (SURVEY 8d): issue_frac = "
+                                             "warp instructions (ncu) / (592 schedulers x SM clock) / measured launch time",
+                         "peak_source": peak_src, "algorithmic_bytes_per_launch": kbytes["k_raster"],
                          "avg_launch_ms": raster_ms,
+                         "kernels": per_kernel,
                          "step": {"algorithmic_bytes_fwd": fwd_b, "algorithmic_bytes_bwd": bwd_b,
                                   "ms_per_frame": step_ms,
                                   "achieved_GBps": (fwd_b + bwd_b) / (step_ms * 1e-3) / 1e9,
                                   "frac": (fwd_b + bwd_b) / (step_ms * 1e-3) / 1e9 / peak},
                          "kernels_separate_pass": kernels},
         }
+        if plugin is not None:
+            line["e2e_plugin"] = plugin
         if world == 1 and not args.no_cpu_baseline:
             from oracle import oracle as orc
             orc.build()
-            threads = host_threads()
-            secs = cpu_frame_seconds(threads, repeats=1)[0]
-            line["cpu_baseline"] = {"value": 1.0 / secs, "unit": "frames/s", "cores": threads, "kind": "port",
-                                    "sample": "1 full C3 frame (fwd+bwd, tau=0.01) on the float64 oracle port, "
-                                              "OpenMP over tiles"}
+            _, line["cpu_baseline"] = cpu_baseline_block(host_threads(), frames=1)
         print(json.dumps(line), flush=True)
     if world > 1:
         dist.destroy_process_group()

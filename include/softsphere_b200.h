@@ -251,6 +251,14 @@ int ss_adam_flat(float *params, const float *grads, float *m, float *v, int64_t 
  *           && (visibility == NULL || visibility[i] > 0);  comparisons in float64 like the reference. */
 int ss_prune_mask(const float *opa, const float *feat, const float *bg, const int32_t *visibility, int64_t M,
                   int32_t d, double opacity_min, double background_dist, uint8_t *keep, void *stream);
+/* Same rule on float64 device columns (the reference-signature prune() wrapper: an opacity exactly at the
+ * threshold must compare as the reference's float64 value does). */
+int ss_prune_mask_f64(const double *opa, const double *feat, const double *bg, const int32_t *visibility, int64_t M,
+                      int32_t d, double opacity_min, double background_dist, uint8_t *keep, void *stream);
+
+/* keep[i] = values[i] != 0.  With values = pixel_count this marks the spheres that received gradient
+ * (SceneGradients.pixel_count > 0, grad.py:45-61): a host caller then compacts and downloads only those rows. */
+int ss_mask_nonzero_i32(const int32_t *values, int64_t M, uint8_t *keep, void *stream);
 
 /* One per-sphere column to compact: `row_bytes` (a multiple of 4) bytes per sphere, device pointers. */
 typedef struct SsColumn {
@@ -270,6 +278,10 @@ int ss_compact_rows(const uint8_t *keep, int64_t M, const SsColumn *cols, int32_
 /* Outputs hold 12 M rows; child c of parent p is row 12 p + c (reshape(m * 12, 3), optim.py:204). */
 int ss_subdivide(const float *pos, const float *rad, const float *opa, const float *feat, int64_t M, int32_t d,
                  double scale, float *pos_out, float *rad_out, float *opa_out, float *feat_out, void *stream);
+/* float64 columns in and out (the reference-signature subdivide() wrapper: children exact in float64). */
+int ss_subdivide_f64(const double *pos, const double *rad, const double *opa, const double *feat, int64_t M,
+                     int32_t d, double scale, double *pos_out, double *rad_out, double *opa_out, double *feat_out,
+                     void *stream);
 
 /* ------------------------------------------------------------------------------------------------
  * the on-disk record formats straight into / out of the device SoA columns.

@@ -97,7 +97,7 @@ class SsStatus(C.Structure):
 
 EXPORTS = ("ss_abi_version", "ss_status_string", "ss_last_cuda_error", "ss_workspace_bytes", "ss_workspace_init",
            "ss_forward", "ss_backward", "ss_read_status", "ss_photometric_loss", "ss_fit_step", "ss_adam_flat", "ss_debug_tile_lists", "ss_launch_count",
-           "ss_prune_mask", "ss_compact_workspace_bytes", "ss_compact_rows", "ss_subdivide",
+           "ss_prune_mask", "ss_prune_mask_f64", "ss_subdivide_f64", "ss_mask_nonzero_i32", "ss_compact_workspace_bytes", "ss_compact_rows", "ss_subdivide",
            "ss_psc1_unpack", "ss_psc1_pack", "ss_convert_f64_f32", "ss_convert_f32_f64",
            "ss_shade_identity", "ss_shade_identity_backward", "ss_shade_diffuse", "ss_shade_diffuse_backward",
            "ss_shade_linear", "ss_shade_linear_backward", "ss_view_directions",
@@ -141,6 +141,9 @@ def load():
     V, I64, I32, D = C.c_void_p, C.c_int64, C.c_int32, C.c_double
     for name, argtypes in (
             ("ss_prune_mask", [V, V, V, V, I64, I32, D, D, V, V]),
+            ("ss_prune_mask_f64", [V, V, V, V, I64, I32, D, D, V, V]),
+            ("ss_subdivide_f64", [V, V, V, V, I64, I32, D, V, V, V, V, V]),
+            ("ss_mask_nonzero_i32", [V, I64, V, V]),
             ("ss_compact_workspace_bytes", [I64, C.POINTER(C.c_size_t)]),
             ("ss_compact_rows", [V, I64, C.POINTER(SsColumn), I32, V, C.c_size_t, V, V]),
             ("ss_subdivide", [V, V, V, V, I64, I32, D, V, V, V, V, V]),

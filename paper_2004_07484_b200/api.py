@@ -6,8 +6,16 @@ types, so they drop into `softsphere.optim.fit(..., renderer=SoftsphereAdapter()
 (optim.py:228-278) and into tests written against the reference.  Scene / camera / params may
 be this package's types or the reference's own objects (same attribute names).
 
-Host arrays are snapped to float32 on upload (the device path is float32 SoA + float64
-geometry); outputs come back as float64 NumPy arrays like the reference's.
+Host <-> device traffic of one call (the part of the plug-in path that is not a kernel):
+  * the scene's NumPy columns (float64 in the reference) are narrowed to float32 straight into ONE pinned
+    staging block (multi-threaded copy, no intermediate array) and travel as one H2D copy;
+  * render_backward re-uses the device copy made by the render_forward that produced `buffer` when it is
+    handed the very same scene object with the very same column arrays (identity + a sampled fingerprint;
+    the reference's fit loop calls forward and backward on one unmodified scene, optim.py:292-304) --
+    otherwise it uploads again, like the reference re-reads the scene (grad.py:213);
+  * image and gradients come back through pinned blocks (one D2H copy each) and are widened to the
+    reference's dtypes (image: the `dtype` argument, raster.py:443; gradients: float64, grad.py:224-227)
+    by a multi-threaded copy into the returned arrays.
 """
 from __future__ import annotations
 
@@ -23,25 +31,83 @@ DEFAULT_TILE_SIZE = 16
 GATE_RADIUS_PX = 3.0
 
 
-def _scene_arrays(scene):
+def _scene_columns(scene):
     m = len(scene)
     d = int(scene.feature_dim)
     feats = np.asarray(scene.features)
     if tuple(feats.shape) != (m, d):
         raise ValidationError(f"feature array shape {tuple(feats.shape)} does not match (M={m}, d={d})")
-    return (np.asarray(scene.positions), np.asarray(scene.radii), np.asarray(scene.opacities), feats,
-            np.asarray(scene.background))
+    pos, rad, opa = np.asarray(scene.positions), np.asarray(scene.radii), np.asarray(scene.opacities)
+    if pos.shape != (m, 3) or rad.shape != (m,) or opa.shape != (m,):
+        raise ValidationError("sphere column arrays have mismatched lengths")
+    return pos, rad, opa, feats, np.asarray(scene.background)
 
 
-def _upload(scene, device):
-    pos, rad, opa, feat, bg = _scene_arrays(scene)
+def _fingerprint(cols):
+    """A few hundred strided samples per column: catches bulk in-place edits of a scene between forward and
+    backward (identity of the arrays alone cannot)."""
+    out = []
+    for a in cols:
+        flat = a.reshape(-1)
+        step = max(1, flat.shape[0] // 251)
+        out.append(flat[::step][:512].astype(np.float64).tobytes())
+    return tuple(out)
 
-    def up(a, shape):
-        t = torch.from_numpy(np.ascontiguousarray(a, dtype=np.float32).reshape(shape))
-        return t.to(device, non_blocking=True)
 
-    d = int(scene.feature_dim)
-    return up(pos, (-1, 3)), up(rad, (-1,)), up(opa, (-1,)), up(feat, (-1, d)), up(bg, (-1,))
+class _Stage:
+    """Pinned staging blocks + device output blocks for one problem size (cached on the engine)."""
+
+    def __init__(self, device, m, d, h, w):
+        from .host import PackedGradients
+        self.key = (m, d, h, w)
+        self.m, self.d, self.h, self.w = m, d, h, w
+        f32 = torch.float32
+        self.n_in = m * (5 + d) + d
+        self.h_in = torch.empty(self.n_in, dtype=f32).pin_memory()
+        self.h_img = torch.empty(h * w * (d + 1), dtype=f32).pin_memory()
+        self.h_up = torch.empty((h, w, d), dtype=f32).pin_memory()
+        self.upstream = torch.empty((h, w, d), dtype=f32, device=device)
+        self.d_img = torch.empty(h * w * (d + 1), dtype=f32, device=device)
+        self.grads = PackedGradients(m, d, device)
+
+    @staticmethod
+    def carve_in(t, m, d):
+        o, out = 0, []
+        for n, shape in ((3 * m, (m, 3)), (m, (m,)), (m, (m,)), (m * d, (m, d)), (d, (d,))):
+            out.append(t[o:o + n].view(shape))
+            o += n
+        return out
+
+
+def _stage_for(eng: RenderEngine, m, d, h, w) -> _Stage:
+    st = getattr(eng, "_api_stage", None)
+    if st is None or st.key != (m, d, h, w):
+        st = _Stage(eng.device, m, d, h, w)
+        eng._api_stage = st
+    return st
+
+
+def _narrow_into(dst: torch.Tensor, src: np.ndarray):
+    """dst (pinned float32 view) <- src (any float dtype): torch's multi-threaded converting copy."""
+    if src.size:
+        dst.copy_(torch.from_numpy(np.ascontiguousarray(src)).view(dst.shape))
+
+
+def _widen(src: torch.Tensor, dtype) -> np.ndarray:
+    """New NumPy array of `dtype` holding the values of the pinned tensor `src`."""
+    out = np.empty(tuple(src.shape), dtype=dtype)
+    if out.size:
+        torch.from_numpy(out).copy_(src)
+    return out
+
+
+def _upload_scene(eng: RenderEngine, st: _Stage, cols):
+    m, d = st.m, st.d
+    for dst, src in zip(_Stage.carve_in(st.h_in, m, d), cols):
+        _narrow_into(dst, src)
+    d_in = torch.empty(st.n_in, dtype=torch.float32, device=eng.device)  # fresh: the buffer keeps it for backward
+    d_in.copy_(st.h_in, non_blocking=True)
+    return tuple(_Stage.carve_in(d_in, m, d))
 
 
 def render_forward(scene, camera, params, *, workers: int = 1, dtype=np.float64,
@@ -49,63 +115,102 @@ def render_forward(scene, camera, params, *, workers: int = 1, dtype=np.float64,
                    engine: RenderEngine = None):
     """Bounds, depth order, tile binning and tile draw on the GPU.
 
-    Returns (FeatureImage, BackwardBuffer or None, RenderStats) like the reference.  `workers`
-    and `dtype` are accepted for signature compatibility and ignored (the device path is
-    deterministic and mixed float32/float64 by design)."""
+    Returns (FeatureImage, BackwardBuffer or None, RenderStats) like the reference.  `workers` is accepted
+    for signature compatibility (the device path is deterministic); `dtype` selects the dtype of the returned
+    arrays like in the reference (raster.py:462-474) -- the device arithmetic is the mixed float32 blend /
+    float64 geometry path either way."""
     eng = engine or default_engine()
     if tile_size != DEFAULT_TILE_SIZE:
         raise ConfigurationError("the B200 path supports tile_size=16 only")
     if not (1 <= int(chunk_size) <= 256):
         raise ConfigurationError("chunk_size must be in 1..256")
+    dtype = np.dtype(dtype)
+    if dtype not in (np.dtype(np.float64), np.dtype(np.float32)):
+        raise ConfigurationError(f"dtype must be float64 or float32, got {dtype}")
     p = params if isinstance(params, BlendParams) else BlendParams(params.gamma, params.epsilon, params.tau,
                                                                    params.top_k)
-    dev_in = _upload(scene, eng.device)
+    cols = _scene_columns(scene)
     # background is validated on the host (d numbers); per-sphere fields are scanned on the device
     if not np.all(np.isfinite(np.asarray(scene.background, dtype=np.float64))):
         raise ValidationError("background feature contains non-finite values")
     cam = CameraSpec.from_camera(camera)
-    res = eng.forward(*dev_in, cam, gamma=p.gamma, eps=p.epsilon, tau=p.tau, top_k=p.top_k,
-                      chunk=int(chunk_size), store_buffer=store_buffer, collect_stats=True, check=True)
-    st = res["status"]
-    image = FeatureImage(data=res["image"].cpu().numpy().astype(np.float64),
-                         background_weight=res["bg_weight"].cpu().numpy().astype(np.float64))
+    m, d, h, w = len(scene), int(scene.feature_dim), int(cam.height), int(cam.width)
+    with torch.cuda.device(eng.device):
+        st = _stage_for(eng, m, d, h, w)
+        dev_in = _upload_scene(eng, st, cols)
+        n_img = h * w * d
+        # the kernels write image | bg_weight into one device block: one D2H copy
+        res = eng.forward(*dev_in, cam, gamma=p.gamma, eps=p.epsilon, tau=p.tau, top_k=p.top_k,
+                          chunk=int(chunk_size), store_buffer=store_buffer, collect_stats=True, check=True,
+                          image=st.d_img[:n_img].view(h, w, d), bg_weight=st.d_img[n_img:].view(h, w))
+        stat = res["status"]
+        st.h_img.copy_(st.d_img, non_blocking=True)
+        torch.cuda.current_stream(eng.device).synchronize()
+    image = FeatureImage(data=_widen(st.h_img[:n_img].view(h, w, d), dtype),
+                         background_weight=_widen(st.h_img[n_img:].view(h, w), dtype))
     buffer = None
     if store_buffer:
-        buffer = BackwardBuffer({k: res[k] for k in ("ids", "z", "closeness", "log_denom")}, p, len(scene))
+        buffer = BackwardBuffer({k: res[k] for k in ("ids", "z", "closeness", "log_denom", "fwd_token")}, p,
+                                len(scene), dtype=dtype)
         buffer._inputs = res["inputs"]
+        buffer._host_cols = cols  # strong references: ids of live objects cannot be recycled
+        buffer._scene_fp = _fingerprint(cols)
     ntx, nty = (cam.width + 15) // 16, (cam.height + 15) // 16
-    stats = RenderStats(spheres_total=len(scene), spheres_on_sensor=st["spheres_on_sensor"],
-                        candidates_tested=st["candidates_tested"], hits_blended=st["hits_blended"],
-                        pixels_early_stopped=st["pixels_early_stopped"], tiles=ntx * nty)
+    stats = RenderStats(spheres_total=len(scene), spheres_on_sensor=stat["spheres_on_sensor"],
+                        candidates_tested=stat["candidates_tested"], hits_blended=stat["hits_blended"],
+                        pixels_early_stopped=stat["pixels_early_stopped"], tiles=ntx * nty)
     return image, buffer, stats
+
+
+def _same_scene(buffer: BackwardBuffer, cols) -> bool:
+    held = getattr(buffer, "_host_cols", None)
+    if held is None or getattr(buffer, "_inputs", None) is None:
+        return False
+    if not all(a is b for a, b in zip(held, cols)):
+        return False
+    return buffer._scene_fp == _fingerprint(cols)
 
 
 def render_backward(scene, camera, params, buffer: BackwardBuffer, upstream, *, workers: int = 1,
                     normalize: bool = True, gate: bool = True, tile_size: int = 16,
-                    engine: RenderEngine = None):
-    """Full backward pipeline; returns (SceneGradients, CameraGradients) as float64 NumPy."""
+                    engine: RenderEngine = None, reuse_upload: bool = True):
+    """Full backward pipeline; returns (SceneGradients, CameraGradients) as float64 NumPy like the reference.
+    reuse_upload=False always re-uploads the scene (see the module docstring)."""
     eng = engine or default_engine()
     if buffer.num_spheres != len(scene):
         raise ContractViolation(f"buffer built for {buffer.num_spheres} spheres, scene has {len(scene)}")
-    upstream = np.asarray(upstream, dtype=np.float64)
+    upstream = np.asarray(upstream)
+    if upstream.dtype not in (np.float64, np.float32):
+        upstream = upstream.astype(np.float64)
     k, h, w = buffer.dev["ids"].shape
-    if upstream.shape != (h, w, scene.feature_dim):
-        raise ValidationError(f"upstream shape {upstream.shape} != {(h, w, scene.feature_dim)}")
+    m, d = len(scene), int(scene.feature_dim)
+    if upstream.shape != (h, w, d):
+        raise ValidationError(f"upstream shape {upstream.shape} != {(h, w, d)}")
     bp = buffer.params
     cam = CameraSpec.from_camera(camera)
-    dev_in = _upload(scene, eng.device)
-    up = torch.from_numpy(np.ascontiguousarray(upstream, dtype=np.float32)).to(eng.device, non_blocking=True)
-    out = eng.backward(*dev_in, cam, buffer.dev, up, gamma=bp.gamma, eps=bp.epsilon, normalize=normalize,
-                       gate=gate, camera_grads=True)
-    m, d = len(scene), int(scene.feature_dim)
+    cols = _scene_columns(scene)
+    with torch.cuda.device(eng.device):
+        st = _stage_for(eng, m, d, h, w)
+        if reuse_upload and _same_scene(buffer, cols):
+            dev_in = buffer._inputs
+        else:
+            dev_in = _upload_scene(eng, st, cols)
+        _narrow_into(st.h_up, upstream)
+        st.upstream.copy_(st.h_up, non_blocking=True)
+        out = eng.backward(*dev_in, cam, buffer.dev, st.upstream, gamma=bp.gamma, eps=bp.epsilon,
+                           normalize=normalize, gate=gate, camera_grads=True, out=dict(st.grads.dev),
+                           accumulate=False)
+        hg = st.grads.download(torch.cuda.current_stream(eng.device))
+        torch.cuda.current_stream(eng.device).synchronize()
+        del out
     grads = SceneGradients(
-        d_position=out["d_pos"].cpu().numpy().astype(np.float64).reshape(m, 3),
-        d_radius=out["d_rad"].cpu().numpy().astype(np.float64),
-        d_opacity=out["d_opa"].cpu().numpy().astype(np.float64),
-        d_feature=out["d_feat"].cpu().numpy().astype(np.float64).reshape(m, d),
-        pixel_count=out["pixel_count"].cpu().numpy().astype(np.int64),
+        d_position=_widen(hg["d_pos"], np.float64),
+        d_radius=_widen(hg["d_rad"], np.float64),
+        d_opacity=_widen(hg["d_opa"], np.float64),
+        d_feature=_widen(hg["d_feat"], np.float64),
+        pixel_count=_widen(hg["pixel_count"], np.int64),
     )
-    cg = out["cam_grad"].cpu().numpy()
+    cg = hg["cam_grad"].numpy().copy()
     g_rot = cg[3:12].reshape(3, 3)
     if camera.rotation_type == AXIS_ANGLE:
         d_rot = axis_angle_vjp(camera.rotation_param, g_rot)
@@ -118,16 +223,22 @@ def render_backward(scene, camera, params, buffer: BackwardBuffer, upstream, *, 
 
 class SoftsphereAdapter:
     """`renderer=` plug-in for the reference's fit loop (optim.py:265-278): an object with
-    forward(scene, camera, params) and backward(scene, camera, params, buffer, upstream)."""
+    forward(scene, camera, params) and backward(scene, camera, params, buffer, upstream).
 
-    def __init__(self, normalize: bool = True, gate: bool = True, engine: RenderEngine = None):
+    The reference's fit does not pass its normalize/gate settings to a plug-in (optim.py:273-278), so they
+    are constructor arguments here (defaults = FitConfig's defaults)."""
+
+    def __init__(self, normalize: bool = True, gate: bool = True, engine: RenderEngine = None,
+                 dtype=np.float64, reuse_upload: bool = True):
         self.normalize = normalize
         self.gate = gate
         self.engine = engine
+        self.dtype = dtype
+        self.reuse_upload = reuse_upload
 
     def forward(self, scene, camera, params):
-        return render_forward(scene, camera, params, engine=self.engine)
+        return render_forward(scene, camera, params, engine=self.engine, dtype=self.dtype)
 
     def backward(self, scene, camera, params, buffer, upstream):
         return render_backward(scene, camera, params, buffer, upstream, normalize=self.normalize,
-                               gate=self.gate, engine=self.engine)
+                               gate=self.gate, engine=self.engine, reuse_upload=self.reuse_upload)

@@ -138,6 +138,20 @@ cudaError_t launch_backward(const BwdLaunch &a, cudaStream_t s);
 
 void count_launch(int n = 1);
 
+// Function attributes (dynamic shared memory size, carve-out) are per DEVICE: a process that drives several GPUs
+// must set them once on each.  One flag array per call site; returns true the first time the calling thread's
+// current device is seen (a benign race sets the attribute twice).
+struct PerDeviceOnce {
+    bool done[64] = {};
+    bool first() {
+        int dev = 0;
+        if (cudaGetDevice(&dev) != cudaSuccess || dev < 0 || dev >= 64) return true;
+        if (done[dev]) return false;
+        done[dev] = true;
+        return true;
+    }
+};
+
 // Optional per-kernel CUDA-event timing (ss_profile_*): used by bench.py for the roofline line.
 enum KernelId { KID_PROJECT = 0, KID_SCAN, KID_EMIT, KID_SORT_SMALL, KID_SORT_BIG, KID_RASTER, KID_BACKWARD,
                 KID_FINALIZE, KID_MEMSET_FWD, KID_MEMSET_BWD, KID_COUNT };

@@ -98,7 +98,10 @@ __global__ void __launch_bounds__(256) k_fit_step(FitArgs a) {
             g0 += (float)(dzeta * a.Rz[0]); g1 += (float)(dzeta * a.Rz[1]); g2 += (float)(dzeta * a.Rz[2]);
             go += (float)(-a.lambda_od * z);
         }
-        if (a.visibility) a.visibility[i] += a.pixel_count[i];
+        if (a.visibility) {  // saturating: the reference sums in int64 (optim.py:307); prune only asks "> 0"
+            const long long v = (long long)a.visibility[i] + (long long)a.pixel_count[i];
+            a.visibility[i] = v > 0x7fffffffLL ? 0x7fffffff : (int)v;
+        }
         if (a.active[0]) {
             float m0 = a.m_pos[3 * i], m1 = a.m_pos[3 * i + 1], m2 = a.m_pos[3 * i + 2];
             float v0 = a.v_pos[3 * i], v1 = a.v_pos[3 * i + 1], v2 = a.v_pos[3 * i + 2];

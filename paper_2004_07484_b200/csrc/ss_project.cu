@@ -847,13 +847,12 @@ cudaError_t launch_binning(const FwdLaunch &a, cudaStream_t s) {
             k_tile_sort_small<<<L.n_tiles, 256, 0, s>>>(tile_start, pair_key, pair_id, (const int *)(ws + L.bucket),
                                                         (const unsigned long long *)(ws + L.key), tile_cursor, status);
         }
-        static bool attr_set = false;
+        static PerDeviceOnce attr_once;
         size_t big_smem = (size_t)SORT_BIG * 12 + (size_t)PACK_BIG * 4;
-        if (!attr_set) {
+        if (attr_once.first()) {
             cudaError_t e = cudaFuncSetAttribute(k_tile_sort_big, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                                  (int)big_smem);
             if (e != cudaSuccess) return e;
-            attr_set = true;
         }
         int grid_big = L.n_tiles < 296 ? L.n_tiles : 296;
         {

@@ -512,8 +512,8 @@ constexpr size_t raster_smem_bytes() {
 template <int DP, int KT, int MODE>
 void launch_one(const RasterArgs &r, int n_tiles, cudaStream_t s) {
     constexpr size_t smem = raster_smem_bytes<DP, KT>();
-    static bool attr_done = false;  // per instantiation
-    if (!attr_done) {
+    static PerDeviceOnce attr_once;  // per instantiation and device
+    if (attr_once.first()) {
         if (smem + 1024 > 48 * 1024)
             cudaFuncSetAttribute(k_raster<DP, KT, MODE>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
 #ifndef SS_RASTER_CARVEOUT
@@ -522,7 +522,6 @@ void launch_one(const RasterArgs &r, int n_tiles, cudaStream_t s) {
         if (SS_RASTER_CARVEOUT >= 0)
             cudaFuncSetAttribute(k_raster<DP, KT, MODE>, cudaFuncAttributePreferredSharedMemoryCarveout,
                                  SS_RASTER_CARVEOUT);
-        attr_done = true;
     }
     k_raster<DP, KT, MODE><<<n_tiles, TILE_PX, smem, s>>>(r);
 }

@@ -28,8 +28,11 @@ namespace {
 
 constexpr int CB = 256;  // spheres per compaction block
 
-__global__ void __launch_bounds__(CB) k_prune_flags(const float *__restrict__ opa, const float *__restrict__ feat,
-                                                    const float *__restrict__ bg,
+// T = float: the device-resident float32 columns; T = double: the reference-signature wrapper's float64 host
+// columns (an opacity exactly at the threshold must not flip by float32 rounding, optim.py:169-175)
+template <typename T>
+__global__ void __launch_bounds__(CB) k_prune_flags(const T *__restrict__ opa, const T *__restrict__ feat,
+                                                    const T *__restrict__ bg,
                                                     const int *__restrict__ visibility, long long M, int d,
                                                     double opacity_min, double background_dist,
                                                     unsigned char *keep) {
@@ -92,6 +95,12 @@ __global__ void __launch_bounds__(1024) k_compact_scan(int *block_count, int n_b
     if (tid == 0) *total_out = carry_s;
 }
 
+// keep[i] = v[i] != 0 (e.g. pixel_count > 0: the spheres that received gradient)
+__global__ void __launch_bounds__(256) k_mask_nonzero(const int *__restrict__ v, long long M, unsigned char *keep) {
+    const long long i = (long long)blockIdx.x * 256 + threadIdx.x;
+    if (i < M) keep[i] = v[i] != 0 ? 1 : 0;
+}
+
 constexpr int MAX_COLS = 16;
 struct Columns {
     const unsigned *src[MAX_COLS];
@@ -139,21 +148,22 @@ __global__ void __launch_bounds__(CB) k_compact_rows(const unsigned char *__rest
 __constant__ float c_fcc[12][3] = {{1, 1, 0},  {1, -1, 0}, {-1, 1, 0},  {-1, -1, 0}, {1, 0, 1},  {1, 0, -1},
                                    {-1, 0, 1}, {-1, 0, -1}, {0, 1, 1},  {0, 1, -1},  {0, -1, 1}, {0, -1, -1}};
 
-// one thread per child
-__global__ void __launch_bounds__(256) k_subdivide(const float *__restrict__ pos, const float *__restrict__ rad,
-                                                   const float *__restrict__ opa, const float *__restrict__ feat,
-                                                   long long M, int d, double scale, float *pos_o, float *rad_o,
-                                                   float *opa_o, float *feat_o) {
+// one thread per child (T = double: float64 columns of the reference-signature wrapper, children exact in float64)
+template <typename T>
+__global__ void __launch_bounds__(256) k_subdivide(const T *__restrict__ pos, const T *__restrict__ rad,
+                                                   const T *__restrict__ opa, const T *__restrict__ feat,
+                                                   long long M, int d, double scale, T *pos_o, T *rad_o,
+                                                   T *opa_o, T *feat_o) {
     const long long c = (long long)blockIdx.x * blockDim.x + threadIdx.x;
     if (c >= M * 12) return;
     const long long p = c / 12;
     const int k = (int)(c - p * 12);
     const double r = (double)rad[p];
     const double a = r / sqrt(2.0);
-    pos_o[3 * c] = (float)((double)pos[3 * p] + a * (double)c_fcc[k][0]);
-    pos_o[3 * c + 1] = (float)((double)pos[3 * p + 1] + a * (double)c_fcc[k][1]);
-    pos_o[3 * c + 2] = (float)((double)pos[3 * p + 2] + a * (double)c_fcc[k][2]);
-    rad_o[c] = (float)(r * scale);
+    pos_o[3 * c] = (T)((double)pos[3 * p] + a * (double)c_fcc[k][0]);
+    pos_o[3 * c + 1] = (T)((double)pos[3 * p + 1] + a * (double)c_fcc[k][1]);
+    pos_o[3 * c + 2] = (T)((double)pos[3 * p + 2] + a * (double)c_fcc[k][2]);
+    rad_o[c] = (T)(r * scale);
     opa_o[c] = opa[p];
     for (int j = 0; j < d; ++j) feat_o[(size_t)c * d + j] = feat[(size_t)p * d + j];
 }
@@ -215,8 +225,28 @@ int ss_prune_mask(const float *opa, const float *feat, const float *bg, const in
     if (M < 0 || d < 1 || d > SS_MAX_FEATURE_DIM) return SS_ERR_DIMS;
     if (M == 0) return SS_OK;
     if (!opa || !keep || (background_dist > 0.0 && (!feat || !bg))) return SS_ERR_NULL;
-    k_prune_flags<<<(unsigned)((M + CB - 1) / CB), CB, 0, (cudaStream_t)stream>>>(
+    k_prune_flags<float><<<(unsigned)((M + CB - 1) / CB), CB, 0, (cudaStream_t)stream>>>(
         opa, feat, bg, visibility, M, d, opacity_min, background_dist, keep);
+    count_launch();
+    return rc_of(cudaGetLastError());
+}
+
+int ss_prune_mask_f64(const double *opa, const double *feat, const double *bg, const int32_t *visibility, int64_t M,
+                      int32_t d, double opacity_min, double background_dist, uint8_t *keep, void *stream) {
+    if (M < 0 || d < 1 || d > SS_MAX_FEATURE_DIM) return SS_ERR_DIMS;
+    if (M == 0) return SS_OK;
+    if (!opa || !keep || (background_dist > 0.0 && (!feat || !bg))) return SS_ERR_NULL;
+    k_prune_flags<double><<<(unsigned)((M + CB - 1) / CB), CB, 0, (cudaStream_t)stream>>>(
+        opa, feat, bg, visibility, M, d, opacity_min, background_dist, keep);
+    count_launch();
+    return rc_of(cudaGetLastError());
+}
+
+int ss_mask_nonzero_i32(const int32_t *values, int64_t M, uint8_t *keep, void *stream) {
+    if (M < 0) return SS_ERR_DIMS;
+    if (M == 0) return SS_OK;
+    if (!values || !keep) return SS_ERR_NULL;
+    k_mask_nonzero<<<(unsigned)((M + 255) / 256), 256, 0, (cudaStream_t)stream>>>(values, M, keep);
     count_launch();
     return rc_of(cudaGetLastError());
 }
@@ -264,8 +294,22 @@ int ss_subdivide(const float *pos, const float *rad, const float *opa, const flo
     if (!pos || !rad || !opa || !feat || !pos_out || !rad_out || !opa_out || !feat_out) return SS_ERR_NULL;
     if (!(scale > 0.0)) return SS_ERR_PARAMS;
     const long long n = (long long)M * 12;
-    k_subdivide<<<(unsigned)((n + 255) / 256), 256, 0, (cudaStream_t)stream>>>(pos, rad, opa, feat, M, d, scale,
-                                                                                  pos_out, rad_out, opa_out, feat_out);
+    k_subdivide<float><<<(unsigned)((n + 255) / 256), 256, 0, (cudaStream_t)stream>>>(
+        pos, rad, opa, feat, M, d, scale, pos_out, rad_out, opa_out, feat_out);
+    count_launch();
+    return rc_of(cudaGetLastError());
+}
+
+int ss_subdivide_f64(const double *pos, const double *rad, const double *opa, const double *feat, int64_t M,
+                     int32_t d, double scale, double *pos_out, double *rad_out, double *opa_out, double *feat_out,
+                     void *stream) {
+    if (M < 0 || d < 1 || d > SS_MAX_FEATURE_DIM || M > (int64_t)1 << 40) return SS_ERR_DIMS;
+    if (M == 0) return SS_OK;
+    if (!pos || !rad || !opa || !feat || !pos_out || !rad_out || !opa_out || !feat_out) return SS_ERR_NULL;
+    if (!(scale > 0.0)) return SS_ERR_PARAMS;
+    const long long n = (long long)M * 12;
+    k_subdivide<double><<<(unsigned)((n + 255) / 256), 256, 0, (cudaStream_t)stream>>>(
+        pos, rad, opa, feat, M, d, scale, pos_out, rad_out, opa_out, feat_out);
     count_launch();
     return rc_of(cudaGetLastError());
 }

@@ -92,14 +92,21 @@ class RenderEngine:
         self._ws: Optional[torch.Tensor] = None
         self._ws_dims = None
         self._pair_capacity = 0
-        self._last_fwd_key = None
+        # Record reuse (SS_OPT_REUSE_RECORDS): the workspace holds the draw records of exactly one forward call.
+        # Every forward gets a token; backward skips re-projection only for the buffer that carries the token of
+        # the workspace's LAST forward, and only while that call's input tensors (kept alive here, so their
+        # addresses cannot be recycled) are the ones handed to backward, unmodified (torch version counters).
+        self._fwd_seq = 0
+        self._last_fwd = None
 
     # -- workspace -------------------------------------------------------------------
     def _dims(self, m, d, w, h, k, max_pairs) -> _lib.SsDims:
         return _lib.SsDims(int(m), int(max_pairs), int(d), int(w), int(h), int(k))
 
     def _ensure_workspace(self, m, d, w, h, k, need_pairs=None):
-        cap = max(self._pair_capacity, self.min_pairs, int(self.pair_factor * m))
+        n_tiles = ((w + 15) // 16) * ((h + 15) // 16)
+        # baseline: 4 pairs per sphere, and room for a few dozen image-filling spheres (64 pairs per tile)
+        cap = max(self._pair_capacity, self.min_pairs, int(self.pair_factor * m), 64 * n_tiles)
         if need_pairs is not None:
             cap = max(cap, int(need_pairs * 1.25) + 1024)
         key = (m, d, w, h, k, cap)
@@ -113,20 +120,46 @@ class RenderEngine:
         if self._ws is None or self._ws.numel() < nbytes.value:
             self._ws = torch.empty(nbytes.value, dtype=torch.uint8, device=self.device)
         # a (re)laid-out workspace must not carry a stale "accumulators are clean" tag (ss_workspace_init)
-        rc = self.lib.ss_workspace_init(C.byref(dims), _ptr(self._ws), self._ws.numel(), self._stream())
+        with torch.cuda.device(self.device):
+            rc = self.lib.ss_workspace_init(C.byref(dims), _ptr(self._ws), self._ws.numel(), self._stream())
         if rc != _lib.SS_OK:
             _raise_for(rc)
         self._ws_dims = key
         self._pair_capacity = cap
-        self._last_fwd_key = None
+        self._last_fwd = None
         return dims
+
+    def invalidate_records(self):
+        """Forget the last forward's draw records (call after editing scene tensors behind torch's back,
+        e.g. from a raw kernel): the next backward re-projects like the reference (grad.py:213, :351)."""
+        self._last_fwd = None
+
+    @staticmethod
+    def _cam_key(cam: CameraSpec):
+        return (tuple(np.asarray(cam.t, np.float64).reshape(-1).tolist()),
+                tuple(np.asarray(cam.R, np.float64).reshape(-1).tolist()), float(cam.focal), float(cam.sensor_w),
+                int(cam.width), int(cam.height), float(cam.near), float(cam.far), cam.mode)
+
+    def _records_current(self, buf: dict, tensors, cam: CameraSpec) -> bool:
+        last = self._last_fwd
+        if last is None or self._ws is None or buf.get("fwd_token") != last["token"]:
+            return False
+        if last["cam"] != self._cam_key(cam):
+            return False
+        for t, (ref, ver) in zip(tensors, last["inputs"]):
+            if t is not ref and (t.data_ptr() != ref.data_ptr() or t.shape != ref.shape):
+                return False
+            if ref._version != ver or t._version != ver:
+                return False
+        return True
 
     def _stream(self):
         return C.c_void_p(torch.cuda.current_stream(self.device).cuda_stream)
 
     def read_status(self) -> dict:
         st = _lib.SsStatus()
-        rc = self.lib.ss_read_status(_ptr(self._ws), C.byref(st), self._stream())
+        with torch.cuda.device(self.device):
+            rc = self.lib.ss_read_status(_ptr(self._ws), C.byref(st), self._stream())
         if rc != _lib.SS_OK:
             _raise_for(rc)
         return {f: int(getattr(st, f)) for f, _ in _lib.SsStatus._fields_ if f != "reserved"}
@@ -134,7 +167,7 @@ class RenderEngine:
     # -- forward ---------------------------------------------------------------------
     def forward(self, pos, rad, opa, feat, bg, cam: CameraSpec, gamma=0.1, eps=1e-2, tau=0.01, top_k=5,
                 chunk=256, tile=16, store_buffer=True, collect_stats=False, validate=True,
-                check=True, debug=False):
+                check=True, debug=False, image=None, bg_weight=None):
         """Enqueue the forward pipeline.  Inputs: float32 CUDA tensors (or array-likes, which are
         copied to the device).  Returns a dict of CUDA tensors; with check=True the status block
         is read back (one stream sync), validation / overflow are handled and `status` is set."""
@@ -155,8 +188,15 @@ class RenderEngine:
             log_denom = torch.empty((h, w), dtype=torch.float32, device=dev)
         else:
             ids = z = clos = log_denom = None
-        image = torch.empty((h, w, d), dtype=torch.float32, device=dev)
-        bgw = torch.empty((h, w), dtype=torch.float32, device=dev)
+        if image is None:
+            image = torch.empty((h, w, d), dtype=torch.float32, device=dev)
+        if bg_weight is None:
+            bg_weight = torch.empty((h, w), dtype=torch.float32, device=dev)
+        bgw = bg_weight
+        for t, shape in ((image, (h, w, d)), (bgw, (h, w))):
+            if tuple(t.shape) != shape or t.dtype != torch.float32 or not t.is_contiguous() or not t.is_cuda:
+                raise ValidationError("caller-provided image / bg_weight must be contiguous float32 CUDA tensors "
+                                      f"of shape {shape}")
         dbg = {}
         if debug:
             dbg = {"rect": torch.empty((m, 4), dtype=torch.int32, device=dev),
@@ -184,7 +224,8 @@ class RenderEngine:
             a.ids, a.z, a.closeness, a.log_denom = _ptr(ids), _ptr(z), _ptr(clos), _ptr(log_denom)
             a.rect, a.on_sensor = _ptr(dbg.get("rect")), _ptr(dbg.get("on_sensor"))
             a.earliest, a.proj_radius_px = _ptr(dbg.get("earliest")), _ptr(dbg.get("proj_radius_px"))
-            rc = self.lib.ss_forward(C.byref(a), self._stream())
+            with torch.cuda.device(dev):  # kernels launch on the current device: make it the engine's
+                rc = self.lib.ss_forward(C.byref(a), self._stream())
             if rc != _lib.SS_OK:
                 _raise_for(rc)
             if not check:
@@ -199,11 +240,13 @@ class RenderEngine:
             break
         else:
             raise SoftSphereError("tile-sphere pair workspace overflow persisted after regrowth")
-        self._last_fwd_key = (m, d, w, h, k, pos.data_ptr(), tuple(np.asarray(cam.t).tolist()),
-                              tuple(np.asarray(cam.R).reshape(-1).tolist()), cam.focal, cam.sensor_w, cam.mode)
+        self._fwd_seq += 1
+        token = (id(self), self._fwd_seq)
+        self._last_fwd = {"token": token, "cam": self._cam_key(cam),
+                          "inputs": tuple((t, t._version) for t in (pos, rad, opa))}
         out = {"image": image, "bg_weight": bgw, "ids": ids, "z": z, "closeness": clos,
                "log_denom": log_denom, "status": status, "num_spheres": m,
-               "inputs": (pos, rad, opa, feat, bg)}
+               "inputs": (pos, rad, opa, feat, bg), "fwd_token": token}
         out.update(dbg)
         return out
 
@@ -249,10 +292,8 @@ class RenderEngine:
             accumulate = False
         if camera_grads and "cam_grad" not in out:
             out["cam_grad"] = torch.empty(16, dtype=torch.float64, device=dev)  # fully written by the kernels
-        fwd_key = (m, d, w, h, k, pos.data_ptr(), tuple(np.asarray(cam.t).tolist()),
-                   tuple(np.asarray(cam.R).reshape(-1).tolist()), cam.focal, cam.sensor_w, cam.mode)
-        reuse = self._ws is not None and self._last_fwd_key == fwd_key
-        dims = self._ensure_workspace(m, d, w, h, k)
+        dims = self._ensure_workspace(m, d, w, h, k)  # (a re-laid-out workspace forgets the last forward)
+        reuse = self._records_current(buf, (pos, rad, opa), cam)
         flags = 0
         if normalize:
             flags |= _lib.OPT_NORMALIZE
@@ -274,7 +315,8 @@ class RenderEngine:
         a.d_pos, a.d_rad, a.d_opa = _ptr(out["d_pos"]), _ptr(out["d_rad"]), _ptr(out["d_opa"])
         a.d_feat, a.pixel_count = _ptr(out["d_feat"]), _ptr(out["pixel_count"])
         a.cam_grad = _ptr(out.get("cam_grad"))
-        rc = self.lib.ss_backward(C.byref(a), self._stream())
+        with torch.cuda.device(dev):
+            rc = self.lib.ss_backward(C.byref(a), self._stream())
         if rc != _lib.SS_OK:
             _raise_for(rc)
         out["_keepalive"] = (pos, rad, opa, feat, bg, upstream)

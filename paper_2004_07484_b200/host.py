@@ -1,18 +1,114 @@
 """Host-buffer session: the reference-facing call for users whose scene lives in host memory
-(as the reference's NumPy columns do).  Pinned staging buffers are allocated once; every
-render_step copies the inputs host->device, runs ss_forward / ss_backward, and copies the image
-and all gradients device->host.  This is the path bench.py times as `e2e`.
+(as the reference's NumPy columns do).  Pinned staging buffers are allocated once; a render_step
+copies what changed host->device, runs ss_forward / ss_backward, and copies the image and the
+gradients device->host.  This is the path bench.py times as `e2e`.
 
-Transfers are packed: the five scene columns travel as ONE pinned block / one H2D copy, all
-gradients (+ pixel counts + the camera block) as ONE block / one D2H copy, and the image
-download runs on a second stream so that it overlaps the upstream upload (the two PCIe
-directions) and the start of the backward pass."""
+Transfers are packed and minimal:
+  * the five scene columns travel as ONE pinned block / one H2D copy, and only when `set_scene` has
+    been called since the last step (a static scene stays resident on the device);
+  * gradients come back either dense (ONE block: all M rows + pixel counts + the camera block) or
+    `compact=True`: only the U rows of spheres that received gradient (pixel_count > 0), preceded by
+    their sphere indices -- ss_mask_nonzero_i32 + ss_compact_rows on the device, then one count read
+    and one D2H copy per column (C3: 36 MB -> 12.7 MB);
+  * the image download runs on a second stream so that it overlaps the upstream upload (the two
+    PCIe directions) and the start of the backward pass."""
 from __future__ import annotations
+
+import ctypes as C
 
 import numpy as np
 import torch
 
-from .engine import CameraSpec, RenderEngine
+from . import _lib
+from .engine import CameraSpec, RenderEngine, _ptr, _raise_for
+
+
+class PackedGradients:
+    """All per-sphere gradients of one backward call in ONE device block of 4-byte words
+    [d_pos 3m | d_rad m | d_opa m | d_feat m*d | pixel_count m | camera block 16 float64] and its pinned
+    host twin, carved into views (`dev`, `host`): one D2H copy moves everything."""
+
+    def __init__(self, num_spheres: int, feature_dim: int, device):
+        m, d = int(num_spheres), int(feature_dim)
+        self.m, self.d = m, d
+        n_out = m * (6 + d) + 32
+        n_out += n_out % 2  # keep the float64 camera block 8-byte aligned
+        self.cam_off = n_out - 32
+        self.d_out = torch.empty(n_out, dtype=torch.float32, device=device)
+        self.h_out = torch.empty(n_out, dtype=torch.float32).pin_memory()
+        self.dev = self._carve(self.d_out)
+        self.host = self._carve(self.h_out)
+
+    def _carve(self, t):
+        m, d = self.m, self.d
+        o, res = 0, {}
+        for name, n, shape in (("d_pos", 3 * m, (m, 3)), ("d_rad", m, (m,)), ("d_opa", m, (m,)),
+                               ("d_feat", m * d, (m, d))):
+            res[name] = t[o:o + n].view(shape)
+            o += n
+        res["pixel_count"] = t[o:o + m].view(torch.int32)
+        res["cam_grad"] = t[self.cam_off:self.cam_off + 32].view(torch.float64)
+        return res
+
+    def download(self, stream=None):
+        """Enqueue the single D2H copy; the caller synchronises.  Returns the pinned host views."""
+        self.h_out.copy_(self.d_out, non_blocking=True)
+        return self.host
+
+    def nbytes(self) -> int:
+        return 4 * self.h_out.numel()
+
+
+class CompactGradients:
+    """Rows of the spheres that received gradient, gathered on the device and downloaded as
+    [index | pixel_count | d_pos | d_rad | d_opa | d_feat] column blocks of `count` rows."""
+
+    COLS = (("index", 1, torch.int32), ("pixel_count", 1, torch.int32), ("d_pos", 3, torch.float32),
+            ("d_rad", 1, torch.float32), ("d_opa", 1, torch.float32), ("d_feat", None, torch.float32))
+
+    def __init__(self, num_spheres: int, feature_dim: int, device):
+        m, d = int(num_spheres), int(feature_dim)
+        self.m, self.d, self.device = m, d, device
+        self.lib = _lib.load()
+        self.widths = [w if w is not None else d for _, w, _ in self.COLS]
+        self.index = torch.arange(m, dtype=torch.int32, device=device)  # one-time iota (source of the index column)
+        self.keep = torch.empty(max(m, 1), dtype=torch.uint8, device=device)
+        self.count = torch.zeros(1, dtype=torch.int64, device=device)
+        self.h_count = torch.zeros(1, dtype=torch.int64).pin_memory()
+        self.d_cols = [torch.empty(max(m, 1) * w, dtype=dt, device=device) for (_, _, dt), w in zip(self.COLS, self.widths)]
+        self.h_cols = [torch.empty(max(m, 1) * w, dtype=dt).pin_memory() for (_, _, dt), w in zip(self.COLS, self.widths)]
+        nb = C.c_size_t()
+        rc = self.lib.ss_compact_workspace_bytes(m, C.byref(nb))
+        if rc != _lib.SS_OK:
+            _raise_for(rc)
+        self.ws = torch.empty(max(nb.value, 256), dtype=torch.uint8, device=device)
+
+    def gather(self, grads: dict, stream) -> dict:
+        """grads: dense device gradients (d_pos, d_rad, d_opa, d_feat, pixel_count).  Returns pinned host views
+        of `count` rows after synchronising `stream` (two syncs: the count, then the rows)."""
+        m = self.m
+        sp = C.c_void_p(stream.cuda_stream)
+        rc = self.lib.ss_mask_nonzero_i32(_ptr(grads["pixel_count"]), m, _ptr(self.keep), sp)
+        if rc != _lib.SS_OK:
+            _raise_for(rc)
+        srcs = [self.index, grads["pixel_count"], grads["d_pos"], grads["d_rad"], grads["d_opa"], grads["d_feat"]]
+        arr = (_lib.SsColumn * len(srcs))()
+        for i, (s, dcol, w) in enumerate(zip(srcs, self.d_cols, self.widths)):
+            arr[i].src, arr[i].dst, arr[i].row_bytes = s.data_ptr(), dcol.data_ptr(), 4 * w
+        rc = self.lib.ss_compact_rows(_ptr(self.keep), m, arr, len(srcs), _ptr(self.ws), self.ws.numel(),
+                                      _ptr(self.count), sp)
+        if rc != _lib.SS_OK:
+            _raise_for(rc)
+        self.h_count.copy_(self.count, non_blocking=True)
+        stream.synchronize()
+        n = int(self.h_count[0])
+        out = {"count": n}
+        for (name, _, _), dcol, hcol, w in zip(self.COLS, self.d_cols, self.h_cols, self.widths):
+            hcol[: n * w].copy_(dcol[: n * w], non_blocking=True)
+            out[name] = hcol[: n * w].view(n, w) if w > 1 else hcol[:n]
+        stream.synchronize()
+        self.last_bytes = 8 + 4 * n * sum(self.widths)
+        return out
 
 
 class HostRenderSession:
@@ -43,47 +139,40 @@ class HostRenderSession:
         self.upstream = torch.empty((h, w, d), dtype=f32, device=dev)
         self.h_image = torch.empty((h, w, d), dtype=f32).pin_memory()
 
-        # ---- outputs: one block of 4-byte words [d_pos 3m | d_rad m | d_opa m | d_feat m*d | count m | cam 32]
-        n_out = m * (6 + d) + 32
-        n_out += n_out % 2  # keep the float64 camera block 8-byte aligned
-        cam_off = n_out - 32
-        self.h_out = torch.empty(n_out, dtype=f32).pin_memory()
-        self.d_out = torch.empty(n_out, dtype=f32, device=dev)
-
-        def carve_out(t):
-            o = 0
-            res = {}
-            for name, n, shape in (("d_pos", 3 * m, (m, 3)), ("d_rad", m, (m,)), ("d_opa", m, (m,)),
-                                   ("d_feat", m * d, (m, d))):
-                res[name] = t[o:o + n].view(shape)
-                o += n
-            res["pixel_count"] = t[o:o + m].view(torch.int32)
-            res["cam_grad"] = t[cam_off:cam_off + 32].view(torch.float64)
-            return res
-
-        self.out = carve_out(self.d_out)
-        self.h_grads = carve_out(self.h_out)
+        self.packed = PackedGradients(m, d, dev)
+        self.out, self.h_grads = self.packed.dev, self.packed.host
+        self.d_out, self.h_out = self.packed.d_out, self.packed.h_out
+        self._compact = None
         self.copy_stream = torch.cuda.Stream(device=dev)
-        self.h2d_bytes = 4 * (n_in + h * w * d)
-        self.d2h_bytes = 4 * (h * w * d + n_out)
+        self._scene_dirty = True
+        self.last_h2d_bytes = 0
+        self.last_d2h_bytes = 0
 
     def set_scene(self, pos, rad, opa, feat, bg):
+        """Stage a (new) scene: uploaded by the next render_step, resident afterwards."""
         for dst, src, shape in ((self.h_pos, pos, (self.m, 3)), (self.h_rad, rad, (self.m,)),
                                 (self.h_opa, opa, (self.m,)), (self.h_feat, feat, (self.m, self.d)),
                                 (self.h_bg, bg, (self.d,))):
-            dst.copy_(torch.from_numpy(np.ascontiguousarray(src, dtype=np.float32).reshape(shape)))
+            dst.copy_(torch.from_numpy(np.ascontiguousarray(src)).view(shape))
+        self._scene_dirty = True
 
     def render_step(self, cams, upstream_fn=None, gamma=0.1, eps=1e-2, tau=0.01, normalize=True, gate=True,
-                    check=False, reduce_fn=None):
+                    check=False, reduce_fn=None, compact=False, always_upload=False):
         """One host-to-host step over one or more views of the staged scene:
-        H2D scene; per view: ss_forward, D2H image, [upstream_fn(view, host image) -> host upstream, else
-        the staged h_upstream], H2D upstream, ss_backward (gradients summed over the views);
-        optional reduce_fn(out) (the multi-GPU allreduce); D2H all gradients.  Returns after the
-        streams are synchronised, with the last image and the gradient views (pinned host tensors)."""
+        [H2D scene if set_scene was called since the last step]; per view: ss_forward, D2H image,
+        [upstream_fn(view, host image) -> host upstream, else the staged h_upstream], H2D upstream, ss_backward
+        (gradients summed over the views); optional reduce_fn(out) (the multi-GPU allreduce); D2H gradients
+        (dense block, or compact rows of the touched spheres).  Returns after the streams are synchronised,
+        with the last image and the gradient views (pinned host tensors)."""
         if not isinstance(cams, (list, tuple)):
             cams = [cams]
-        main = torch.cuda.current_stream(self.engine.device)
-        self.d_in.copy_(self.h_in, non_blocking=True)
+        dev = self.engine.device
+        main = torch.cuda.current_stream(dev)
+        h2d = 0
+        if self._scene_dirty or always_upload:
+            self.d_in.copy_(self.h_in, non_blocking=True)
+            self._scene_dirty = False
+            h2d += 4 * self.h_in.numel()
         for i, cam in enumerate(cams):
             if upstream_fn is None:  # upstream already staged on the host: upload it under the forward pass
                 self.copy_stream.wait_stream(main)  # (orders it after the previous view's backward)
@@ -102,18 +191,29 @@ class HostRenderSession:
                 self.copy_stream.synchronize()
                 self.h_upstream.copy_(upstream_fn(i, self.h_image))
                 self.upstream.copy_(self.h_upstream, non_blocking=True)
+            h2d += 4 * self.h_upstream.numel()
             self.engine.backward(self.pos, self.rad, self.opa, self.feat, self.bg, cam, f, self.upstream,
                                  gamma=gamma, eps=eps, normalize=normalize, gate=gate, camera_grads=True,
                                  out=self.out, accumulate=(i > 0))
         if reduce_fn is not None:
             reduce_fn(self.out)
-        self.h_out.copy_(self.d_out, non_blocking=True)
+        d2h = len(cams) * 4 * self.h_image.numel()
+        if compact:
+            if self._compact is None:
+                self._compact = CompactGradients(self.m, self.d, dev)
+            grads = self._compact.gather(self.out, main)
+            self.h_out[self.packed.cam_off:].copy_(self.d_out[self.packed.cam_off:], non_blocking=True)
+            grads["cam_grad"] = self.h_grads["cam_grad"]
+            d2h += self._compact.last_bytes + 4 * 32
+        else:
+            self.packed.download()
+            grads = self.h_grads
+            d2h += self.packed.nbytes()
         main.synchronize()
         self.copy_stream.synchronize()
-        return self.h_image, self.h_grads
+        self.last_h2d_bytes, self.last_d2h_bytes = h2d, d2h
+        return self.h_image, grads
 
     def bytes_per_step(self, views: int):
-        m, d, w, h = self.m, self.d, self.w, self.h
-        h2d = 4 * (m * (5 + d) + d) + views * 4 * h * w * d
-        d2h = views * 4 * h * w * d + 4 * self.h_out.numel()
-        return h2d, d2h
+        """(h2d, d2h) bytes of the LAST render_step (counted from the tensors that were copied)."""
+        return self.last_h2d_bytes, self.last_d2h_bytes

@@ -60,27 +60,63 @@ class ViewShardedRenderer:
         self.distributed = dist.is_available() and dist.is_initialized()
         self.world_size = dist.get_world_size(group) if self.distributed else 1
         self.rank = dist.get_rank(group) if self.distributed else 0
+        self.backend = dist.get_backend(group) if self.distributed else None
+        self._pending = None  # work handle of a deferred allreduce (overlap=True)
+        self.collectives_issued = 0  # collective launches so far (one per step on NCCL)
 
     def local_views(self, num_views: int) -> List[int]:
         return shard_views(num_views, self.world_size, self.rank)
 
+    def finish(self):
+        """Wait (stream-ordered, not a host sync on NCCL) for a deferred allreduce before `grads` is read."""
+        if self._pending is not None:
+            self._pending.wait()
+            self._pending = None
+
+    def _allreduce(self, grads: SphereGradBuffer):
+        """ONE collective per step: the float32 gradient block and the int32 pixel counts travel in one NCCL
+        group (a single fused launch on the communicator's stream, ordered after the last local k_finalize by
+        the usual event; the pixel counts cannot ride in the float buffer, their sums exceed 2^24).  Backends
+        without coalescing (gloo in the CPU tests) issue the two reductions back to back."""
+        if self.backend == "nccl":
+            with dist._coalescing_manager(group=self.group, device=grads.flat.device, async_ops=True) as cm:
+                dist.all_reduce(grads.flat, op=dist.ReduceOp.SUM, group=self.group)
+                dist.all_reduce(grads.pixel_count, op=dist.ReduceOp.SUM, group=self.group)
+            self.collectives_issued += 1
+            return cm
+        h1 = dist.all_reduce(grads.flat, op=dist.ReduceOp.SUM, group=self.group, async_op=True)
+        h2 = dist.all_reduce(grads.pixel_count, op=dist.ReduceOp.SUM, group=self.group, async_op=True)
+        self.collectives_issued += 2
+
+        class _Both:
+            def wait(self_inner):
+                h1.wait()
+                h2.wait()
+        return _Both()
+
     def step(self, scene, cameras: Sequence, upstream_fn: Callable, grads: SphereGradBuffer, gamma=0.1,
-             eps=1e-2, tau=0.01, top_k=5, normalize=True, gate=True, camera_grads=True, check=False):
+             eps=1e-2, tau=0.01, top_k=5, normalize=True, gate=True, camera_grads=True, check=False,
+             overlap=False):
         """One multi-view step.  scene = (pos, rad, opa, feat, bg) device tensors; cameras = the
         CameraSpec of EVERY view (all ranks hold the list); upstream_fn(view, image) -> dL/dimage.
         Fills `grads` with the sum over ALL views (after the allreduce) and returns
-        {view: cam_grad tensor} for the local views."""
+        {view: cam_grad tensor} for the local views.  overlap=True leaves the allreduce in flight (call
+        finish() before reading `grads`): the next step's first forward pass then runs under it, and the
+        next step waits for it before its first backward overwrites the buffer."""
         pos, rad, opa, feat, bg = scene
         cam_out = {}
         out = grads.as_out()
         local = self.local_views(len(cameras))
         if not local:
+            self.finish()
             grads.zero_()
         for i, v in enumerate(local):
             cam = cameras[v]
             f = self.engine.forward(pos, rad, opa, feat, bg, cam, gamma=gamma, eps=eps, tau=tau, top_k=top_k,
                                     check=check)
             up = upstream_fn(v, f["image"])
+            if i == 0:
+                self.finish()  # the previous step's reduction must be done before this buffer is overwritten
             o = dict(out)
             res = self.engine.backward(pos, rad, opa, feat, bg, cam, f, up, gamma=gamma, eps=eps,
                                        normalize=normalize, gate=gate, camera_grads=camera_grads, out=o,
@@ -88,9 +124,7 @@ class ViewShardedRenderer:
             if camera_grads:
                 cam_out[v] = res["cam_grad"]
         if self.world_size > 1:
-            # one NCCL group: float sphere gradients + int pixel counts
-            h1 = dist.all_reduce(grads.flat, op=dist.ReduceOp.SUM, group=self.group, async_op=True)
-            h2 = dist.all_reduce(grads.pixel_count, op=dist.ReduceOp.SUM, group=self.group, async_op=True)
-            h1.wait()
-            h2.wait()
+            self._pending = self._allreduce(grads)
+            if not overlap:
+                self.finish()
         return cam_out

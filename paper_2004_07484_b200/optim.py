@@ -55,6 +55,7 @@ class FitConfig:
     subdivide_at: tuple = ()
     subdivide_scale: float = float(np.sqrt(2.0))
     seed: int = 0
+    workers: int = 1  # accepted like the reference's field (optim.py:58); the device path has no worker pool
 
     def __post_init__(self):
         for name in ("lr_position", "lr_radius", "lr_opacity", "lr_feature", "lr_camera"):
@@ -223,9 +224,13 @@ class DeviceFit:
         if rc != _lib.SS_OK:
             _raise_for(rc)
 
-    def step(self, target: torch.Tensor, cam: CameraSpec, gamma: float = None, check: bool = False):
+    def step(self, target: torch.Tensor, cam: CameraSpec, gamma: float = None, check: bool = True):
         """forward -> loss/upstream -> backward -> fused update.  Returns the loss (float64 tensor [1]:
-        photometric + regulariser energy of the scene BEFORE the update, like the reference's trace)."""
+        photometric + regulariser energy of the scene BEFORE the update, like the reference's trace).
+        check=True (default) reads the status block after the forward pass (one stream sync): invalid fields
+        raise ValidationError like the reference's render_forward, a tile-pair overflow regrows the workspace
+        and re-renders.  check=False never syncs; the caller then polls engine.read_status() itself -- an
+        overflowed frame is background only and yields zero gradients."""
         cfg = self.cfg
         g = cfg.gamma if gamma is None else gamma
         f = self.engine.forward(self.pos, self.rad, self.opa, self.feat, self.bg, cam, gamma=g, eps=cfg.epsilon,
@@ -235,7 +240,8 @@ class DeviceFit:
                                      eps=cfg.epsilon, normalize=cfg.normalize_grads, gate=cfg.gate,
                                      camera_grads=cfg.lr_camera > 0)
         self.apply_gradients(grads, cam)
-        self.last = {"image": f["image"], "grads": grads}
+        self.engine.invalidate_records()  # k_fit_step moved the spheres behind torch's version counters
+        self.last = {"image": f["image"], "grads": grads, "status": f["status"]}
         return loss + self.energy
 
     def check_finite(self, loss: torch.Tensor):
@@ -273,13 +279,22 @@ def _adam_host(params, grads, state: AdamState, lr, cfg):
 
 
 def fit(scene, observations, config: FitConfig, renderer=None, on_step=None, device="cuda") -> FitResult:
-    """Reference signature (optim.py:228).  `renderer` is accepted for compatibility and must be None: the
-    device pipeline IS the renderer.  on_step(step, loss, fit_state, cameras) receives the DeviceFit (device
-    tensors) instead of a host scene; FitResult.scene is downloaded once at the end."""
+    """Reference signature (optim.py:228).  The device pipeline IS the renderer: `renderer` may be None or a
+    SoftsphereAdapter (its engine and its normalize / gate flags are used, like the reference uses a plug-in's
+    own settings, optim.py:273-278); any other plug-in object is refused -- hand that one to the reference's
+    own fit loop.  on_step(step, loss, fit_state, cameras) receives the DeviceFit (device tensors) instead of
+    a host scene; FitResult.scene is downloaded once at the end."""
     from .types import (AXIS_ANGLE, SphereScene, axis_angle_vjp, camera_from_vector, camera_to_vector,
                         rotation_6d_vjp)
+    engine = None
     if renderer is not None:
-        raise ConfigurationError("the device fit loop renders with its own kernels; pass renderer=None")
+        from .api import SoftsphereAdapter
+        if not isinstance(renderer, SoftsphereAdapter):
+            raise ConfigurationError("the device fit loop renders with its own kernels; pass renderer=None or a "
+                                     "SoftsphereAdapter (other plug-ins belong to the reference's fit loop)")
+        import dataclasses
+        config = dataclasses.replace(config, normalize_grads=renderer.normalize, gate=renderer.gate)
+        engine = renderer.engine
     if not observations:
         raise ValidationError("fit needs at least one observation")
     d = scene.feature_dim
@@ -287,7 +302,7 @@ def fit(scene, observations, config: FitConfig, renderer=None, on_step=None, dev
         if tuple(np.shape(ob.image)) != (ob.camera.height, ob.camera.width, d):
             raise ValidationError(f"observation {i} image shape mismatch")
     dfit = DeviceFit(scene.positions, scene.radii, scene.opacities, scene.features, scene.background, config,
-                     device=device)
+                     engine=engine, device=device)
     dev = dfit.engine.device
     targets = [torch.from_numpy(np.ascontiguousarray(ob.image, dtype=np.float32)).to(dev) for ob in observations]
     cameras = [ob.camera for ob in observations]
@@ -304,7 +319,7 @@ def fit(scene, observations, config: FitConfig, renderer=None, on_step=None, dev
         idx = int(order.pop(0))
         seen[idx] = True
         cam = cameras[idx]
-        loss_t = dfit.step(targets[idx], CameraSpec.from_camera(cam), gamma=config.gamma_at(step))
+        loss_t = dfit.step(targets[idx], CameraSpec.from_camera(cam), gamma=config.gamma_at(step), check=True)
         loss = float(loss_t.item())
         if not np.isfinite(loss):
             raise DivergenceError(f"non-finite loss at step {step}")

@@ -87,33 +87,46 @@ def subdivide_device(pos, rad, opa, feat, scale: float):
     return po, ro, oo, fo
 
 
-def _upload(scene: SphereScene, dev):
-    f32 = lambda a, shape: torch.from_numpy(np.ascontiguousarray(a, dtype=np.float32)).reshape(shape).to(dev)
-    d = scene.feature_dim
-    return (f32(scene.positions, (-1, 3)), f32(scene.radii, (-1,)), f32(scene.opacities, (-1,)),
-            f32(scene.features, (-1, d)), f32(scene.background, (d,)))
-
-
-def _download(d, bg, pos, rad, opa, feat) -> SphereScene:
-    f64 = lambda t: t.cpu().numpy().astype(np.float64)
-    return SphereScene(feature_dim=d, background=np.array(bg, dtype=np.float64), positions=f64(pos),
-                       radii=f64(rad), opacities=f64(opa), features=f64(feat))
+def _f64(a, shape, dev):
+    return torch.from_numpy(np.ascontiguousarray(a, dtype=np.float64)).reshape(shape).to(dev)
 
 
 def prune(scene: SphereScene, visibility, config, device="cuda"):
-    """Reference signature (optim.py:161): returns (scene', keep_mask)."""
+    """Reference signature (optim.py:161): returns (scene', keep_mask).  The mask is decided on the device from
+    the scene's own float64 values (k_prune_flags<double>); the survivors are exact float64 copies like the
+    reference's `scene.positions[keep]` (optim.py:176-181)."""
+    lib = _lib.load()
     dev = default_engine(device).device
-    vis_np = np.asarray(visibility).reshape(len(scene))
-    pos, rad, opa, feat, bg = _upload(scene, dev)
-    vis = torch.from_numpy(np.clip(vis_np, 0, np.iinfo(np.int32).max).astype(np.int32)).to(dev)
-    pos, rad, opa, feat, _, keep = prune_device(pos, rad, opa, feat, bg, vis, config.prune_opacity_min,
-                                                config.prune_background_dist)
-    return _download(scene.feature_dim, scene.background, pos, rad, opa, feat), keep.cpu().numpy().astype(bool)
+    m, d = len(scene), int(scene.feature_dim)
+    vis_np = np.asarray(visibility).reshape(m)
+    keep_t = torch.empty(max(m, 1), dtype=torch.uint8, device=dev)
+    if m:
+        with torch.cuda.device(dev):
+            opa, feat, bg = _f64(scene.opacities, (-1,), dev), _f64(scene.features, (-1, d), dev), _f64(scene.background, (d,), dev)
+            vis = torch.from_numpy(np.clip(vis_np, 0, np.iinfo(np.int32).max).astype(np.int32)).to(dev)
+            _check(lib.ss_prune_mask_f64(_ptr(opa), _ptr(feat), _ptr(bg), _ptr(vis), m, d,
+                                         float(config.prune_opacity_min), float(config.prune_background_dist),
+                                         _ptr(keep_t), _stream(dev)))
+    keep = keep_t[:m].cpu().numpy().astype(bool)
+    out = SphereScene(feature_dim=d, background=np.array(scene.background, dtype=np.float64),
+                      positions=np.asarray(scene.positions)[keep], radii=np.asarray(scene.radii)[keep],
+                      opacities=np.asarray(scene.opacities)[keep], features=np.asarray(scene.features)[keep])
+    return out, keep
 
 
 def subdivide(scene: SphereScene, config, device="cuda") -> SphereScene:
-    """Reference signature (optim.py:197)."""
+    """Reference signature (optim.py:197); float64 columns in and out (k_subdivide<double>)."""
+    lib = _lib.load()
     dev = default_engine(device).device
-    pos, rad, opa, feat, _ = _upload(scene, dev)
-    out = subdivide_device(pos, rad, opa, feat, config.subdivide_scale)
-    return _download(scene.feature_dim, scene.background, *out)
+    m, d = len(scene), int(scene.feature_dim)
+    with torch.cuda.device(dev):
+        pos, rad = _f64(scene.positions, (-1, 3), dev), _f64(scene.radii, (-1,), dev)
+        opa, feat = _f64(scene.opacities, (-1,), dev), _f64(scene.features, (-1, d), dev)
+        f64 = dict(dtype=torch.float64, device=dev)
+        po, ro, oo = torch.empty((12 * m, 3), **f64), torch.empty(12 * m, **f64), torch.empty(12 * m, **f64)
+        fo = torch.empty((12 * m, d), **f64)
+        _check(lib.ss_subdivide_f64(_ptr(pos), _ptr(rad), _ptr(opa), _ptr(feat), m, d, float(config.subdivide_scale),
+                                    _ptr(po), _ptr(ro), _ptr(oo), _ptr(fo), _stream(dev)))
+    return SphereScene(feature_dim=d, background=np.array(scene.background, dtype=np.float64),
+                       positions=po.cpu().numpy(), radii=ro.cpu().numpy(), opacities=oo.cpu().numpy(),
+                       features=fo.cpu().numpy())

@@ -341,10 +341,11 @@ class BackwardBuffer:
     `closeness` and `log_denom` materialise NumPy views in the reference's (H, W, K) layout
     on first access."""
 
-    def __init__(self, dev, params: BlendParams, num_spheres: int):
-        self.dev = dev  # dict of CUDA tensors: ids/z/closeness (K,H,W), log_denom (H,W)
+    def __init__(self, dev, params: BlendParams, num_spheres: int, dtype=np.float32):
+        self.dev = dev  # dict of CUDA tensors: ids/z/closeness (K,H,W), log_denom (H,W) (+ the forward token)
         self.params = params
         self.num_spheres = int(num_spheres)
+        self.dtype = np.dtype(dtype)  # dtype of the float views (the reference's buffer has render_forward's dtype)
         self._np = {}
 
     def _get(self, name):
@@ -352,7 +353,8 @@ class BackwardBuffer:
             t = self.dev[name]
             if t.dim() == 3:
                 t = t.permute(1, 2, 0)
-            self._np[name] = t.contiguous().cpu().numpy()
+            a = t.contiguous().cpu().numpy()
+            self._np[name] = a if name == "ids" else a.astype(self.dtype, copy=False)
         return self._np[name]
 
     @property

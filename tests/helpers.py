@@ -59,9 +59,63 @@ def assert_close(actual, expected, rtol, atol, what=""):
                              f"got {a[i]!r}, want {e[i]!r}, err {err[i]:.3e}")
 
 
-def grad_close(actual, expected, what="", rtol=GRAD_RTOL, floor=1e-7):
-    """1e-4 relative with an absolute floor tied to the array's magnitude (float32 atomics
-    reorder sums; gradients of one sphere are sums of cancelling per-pixel terms)."""
+GRAD_SIG = 1e-3      # grad_error reports relative errors of the elements above GRAD_SIG * max|expected|
+GRAD_FLOOR = 2e-6    # absolute floor of grad_close, as a fraction of max|expected|
+
+
+def grad_error(actual, expected, sig=GRAD_SIG):
+    """Per-element error summary of a gradient array against the float64 oracle: relative error of the
+    significant elements (|expected| > sig * max|expected|), absolute error of the rest in units of the max."""
+    a = np.asarray(actual, dtype=np.float64).reshape(-1)
+    e = np.asarray(expected, dtype=np.float64).reshape(-1)
+    if e.size == 0 or not np.any(e):
+        return {"n": int(e.size), "n_sig": 0, "max_rel_sig": 0.0, "p999_rel_sig": 0.0, "p50_rel_sig": 0.0,
+                "max_abs_over_scale": float(np.abs(a - e).max()) if e.size else 0.0}
+    scale = float(np.abs(e).max())
+    big = np.abs(e) > sig * scale
+    rel = np.abs(a - e)[big] / np.abs(e)[big]
+    q = lambda x, p: float(np.quantile(x, p)) if x.size else 0.0
+    return {"n": int(e.size), "n_sig": int(big.sum()), "max_rel_sig": float(rel.max()) if rel.size else 0.0,
+            "p999_rel_sig": q(rel, 0.999), "p50_rel_sig": q(rel, 0.5),
+            "max_abs_over_scale": float(np.abs(a - e).max() / scale)}
+
+
+def grad_close(actual, expected, what="", rtol=GRAD_RTOL, floor=GRAD_FLOOR):
+    """north_star gradient bar: 1e-4 RELATIVE to the float64 oracle, with an absolute floor of 2e-6 of the
+    array's largest magnitude -- i.e. every element above 2 % of the max is held to 1e-4 relative.  The floor is
+    the measured float32 limit of the path, not slack: the backward re-creates the blend weights from a float32
+    buffer (z, closeness, log_denom carry ~1e-6 relative error into exp(o z / gamma - log_denom)) and a sphere's
+    gradient is a sum of ~30 per-pixel terms of both signs, so small elements inherit an ABSOLUTE error of
+    ~1e-6 of the scale (measured worst case over C2 / C3 / reduced C5: 1.1e-6; grad_error() prints the
+    distribution; the reference's own float32 mode is specified to 1e-2)."""
+    a = np.asarray(actual, dtype=np.float64)
     e = np.asarray(expected, dtype=np.float64)
-    scale = float(np.abs(e).max()) if e.size else 0.0
-    assert_close(actual, e, rtol, max(floor, rtol * scale * 0.05), what)
+    assert a.shape == e.shape, f"{what}: shape {a.shape} vs {e.shape}"
+    if a.size == 0:
+        return
+    scale = float(np.abs(e).max())
+    err = np.abs(a - e)
+    tol = np.maximum(rtol * np.abs(e), floor * scale) + 1e-30
+    bad = err > tol
+    if bad.any():
+        i = np.unravel_index(np.argmax(err / tol), err.shape)
+        raise AssertionError(f"{what}: {int(bad.sum())}/{a.size} outside rtol {rtol:g} / floor {floor:g} x max; worst at "
+                             f"{i}: got {a[i]!r}, want {e[i]!r}, err {err[i]:.3e}, array max {scale:.3e}; "
+                             f"summary {grad_error(a, e)}")
+
+
+def reference_package():
+    """The UNMODIFIED reference package, if the driver hook installed it into the git-ignored baseline/_ref
+    (`__graft_entry__.build()` does, from /root/reference, where that exists).  Never read from /root/reference
+    at test time: that path does not exist on the GPU box."""
+    import importlib
+    import sys
+    ref_dir = os.path.join(ROOT, "baseline", "_ref")
+    if not os.path.isdir(os.path.join(ref_dir, "softsphere")):
+        return None
+    if ref_dir not in sys.path:
+        sys.path.append(ref_dir)
+    try:
+        return importlib.import_module("softsphere")
+    except Exception:
+        return None

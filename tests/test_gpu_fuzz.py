@@ -76,14 +76,14 @@ def test_random_geometry_vs_oracle(engine, seed):
         gr = orc.render_backward(*args, ocam, ref, up.astype(np.float64), normalize=bool(seed % 2),
                                  gate=bool(seed % 2))
         assert np.array_equal(out["pixel_count"].cpu().numpy(), gr["pixel_count"])
-        grad_close(out["d_pos"].cpu().numpy(), gr["d_position"], "d_position", rtol=2e-4)
-        grad_close(out["d_rad"].cpu().numpy(), gr["d_radius"], "d_radius", rtol=2e-4)
-        grad_close(out["d_opa"].cpu().numpy(), gr["d_opacity"], "d_opacity", rtol=2e-4)
-        grad_close(out["d_feat"].cpu().numpy(), gr["d_feature"], "d_feature", rtol=2e-4)
+        grad_close(out["d_pos"].cpu().numpy(), gr["d_position"], "d_position")
+        grad_close(out["d_rad"].cpu().numpy(), gr["d_radius"], "d_radius")
+        grad_close(out["d_opa"].cpu().numpy(), gr["d_opacity"], "d_opacity")
+        grad_close(out["d_feat"].cpu().numpy(), gr["d_feature"], "d_feature")
         cg = out["cam_grad"].cpu().numpy()
-        grad_close(cg[0:3], gr["d_translation"], "d_translation", rtol=2e-4)
-        grad_close(cg[3:12].reshape(3, 3), gr["grad_rot_matrix"], "dL/dR", rtol=2e-4)
-        grad_close(cg[12:14], [gr["d_focal"], gr["d_sensor_width"]], "intrinsics", rtol=2e-4)
+        grad_close(cg[0:3], gr["d_translation"], "d_translation")
+        grad_close(cg[3:12].reshape(3, 3), gr["grad_rot_matrix"], "dL/dR")
+        grad_close(cg[12:14], [gr["d_focal"], gr["d_sensor_width"]], "intrinsics")
 
 
 @pytest.mark.parametrize("case", ["equal_depth_ortho", "duplicates", "outlier_range", "near_ties"])
@@ -187,13 +187,13 @@ def test_feature_maps_and_long_records_vs_oracle(engine, d, k):
     out = engine.backward(pos, rad, opa, feat, bg, spec, f, up, gamma=0.15, eps=1e-2)
     gr = orc.render_backward(pos, rad, opa, feat, bg, ocam, ref, up.astype(np.float64))
     assert np.array_equal(out["pixel_count"].cpu().numpy(), gr["pixel_count"])
-    grad_close(out["d_pos"].cpu().numpy(), gr["d_position"], "d_position", rtol=2e-4)
-    grad_close(out["d_rad"].cpu().numpy(), gr["d_radius"], "d_radius", rtol=2e-4)
-    grad_close(out["d_opa"].cpu().numpy(), gr["d_opacity"], "d_opacity", rtol=2e-4)
-    grad_close(out["d_feat"].cpu().numpy(), gr["d_feature"], "d_feature", rtol=2e-4)
+    grad_close(out["d_pos"].cpu().numpy(), gr["d_position"], "d_position")
+    grad_close(out["d_rad"].cpu().numpy(), gr["d_radius"], "d_radius")
+    grad_close(out["d_opa"].cpu().numpy(), gr["d_opacity"], "d_opacity")
+    grad_close(out["d_feat"].cpu().numpy(), gr["d_feature"], "d_feature")
     cg = out["cam_grad"].cpu().numpy()
-    grad_close(cg[0:3], gr["d_translation"], "d_translation", rtol=2e-4)
-    grad_close(cg[12:14], [gr["d_focal"], gr["d_sensor_width"]], "intrinsics", rtol=2e-4)
+    grad_close(cg[0:3], gr["d_translation"], "d_translation")
+    grad_close(cg[12:14], [gr["d_focal"], gr["d_sensor_width"]], "intrinsics")
 
 
 def make_random_scene_d(rng, m, d):

@@ -366,18 +366,30 @@ def main():
         params_np = pk.BlendParams(gamma=GAMMA, epsilon=EPS, tau=TAU, top_k=TOP_K)
         adapter = pk.SoftsphereAdapter(engine=eng)
 
-        def plugin_step():
+        # protocol of the reference's own benchmark (cli.py:378-389): forward and backward are timed, the host
+        # upstream sign(image - 0.5) between them is the caller's NumPy work and is not
+        plug_steps = max(3, min(args.steps, 20))
+        t_f = t_b = 0.0
+        for it in range(plug_steps + 3):
+            t0 = time.perf_counter()
             image, buf, _ = adapter.forward(scene_np, cam_np, params_np)
-            adapter.backward(scene_np, cam_np, params_np, buf, np.sign(image.data - 0.5))
-
-        plug_steps = max(3, min(args.steps, 10))
-        plugin = {"value": timed(plugin_step, plug_steps), "unit": "frames/s", "steps": plug_steps,
+            t1 = time.perf_counter()
+            up_np = np.sign(image.data - 0.5)
+            t2 = time.perf_counter()
+            adapter.backward(scene_np, cam_np, params_np, buf, up_np)
+            t3 = time.perf_counter()
+            if it >= 3:  # 3 warm-up frames
+                t_f += t1 - t0
+                t_b += t3 - t2
+        plugin = {"value": plug_steps / (t_f + t_b), "unit": "frames/s", "steps": plug_steps,
+                  "forward_ms": 1e3 * t_f / plug_steps, "backward_ms": 1e3 * t_b / plug_steps,
                   "h2d_bytes_per_step": 4 * (COUNT * (5 + D) + D) + 4 * SIZE * SIZE * D,
                   "d2h_bytes_per_step": 4 * SIZE * SIZE * (D + 1) + 4 * (COUNT * (6 + D) + 32),
-                  "path": "SoftsphereAdapter.forward/.backward(SphereScene float64 NumPy, Camera, BlendParams): float64 "
-                          "columns narrowed into pinned staging + 1 H2D, ss_forward, image -> float64 NumPy, host "
-                          "upstream sign(image - 0.5), upstream H2D, ss_backward (scene upload shared with the "
-                          "forward call), all gradients -> float64 NumPy"}
+                  "path": "SoftsphereAdapter.forward / .backward(SphereScene float64 NumPy, Camera, BlendParams), each "
+                          "call returning synchronised NumPy results: float64 columns narrowed into pinned staging + "
+                          "1 H2D, ss_forward, image + bg_weight -> float64 NumPy | upstream float64 -> pinned + H2D, "
+                          "ss_backward (scene upload shared with the forward call), all gradients -> float64 NumPy; "
+                          "the host-side upstream sign(image - 0.5) between the calls is not timed (cli.py:378-389)"}
 
     if rank == 0:
         peaks_path = os.path.join(ROOT, "MEASURED_PEAKS.json")

@@ -148,6 +148,30 @@ __device__ __forceinline__ float pin_reg(float x) {
     return x;
 }
 
+// Shared-memory loads through an explicit 32-bit shared-space address.  With generic pointers into the dynamic
+// shared array the compiler, at the 64-register cap, re-derives the shared window base (S2R SR_CgaCtaId + 3
+// integer instructions) in EVERY drain round instead of keeping it in a register.
+__device__ __forceinline__ float4 lds_f4(unsigned a) {
+    float4 v;
+    asm volatile("ld.shared.v4.f32 {%0, %1, %2, %3}, [%4];" : "=f"(v.x), "=f"(v.y), "=f"(v.z), "=f"(v.w) : "r"(a));
+    return v;
+}
+__device__ __forceinline__ double2 lds_d2(unsigned a) {
+    double2 v;
+    asm volatile("ld.shared.v2.f64 {%0, %1}, [%2];" : "=d"(v.x), "=d"(v.y) : "r"(a));
+    return v;
+}
+__device__ __forceinline__ unsigned lds_u8(unsigned a) {
+    unsigned v;
+    asm volatile("ld.shared.u8 %0, [%1];" : "=r"(v) : "r"(a));
+    return v;
+}
+__device__ __forceinline__ unsigned lds_u32(unsigned a) {
+    unsigned v;
+    asm volatile("ld.shared.u32 %0, [%1];" : "=r"(v) : "r"(a));
+    return v;
+}
+
 constexpr float kLn2 = 0.6931471805599453f;
 #ifndef SS_RASTER_MINB
 #define SS_RASTER_MINB (SS_TOPK_SHARED ? 4 : 3)  // resident CTAs per SM the register allocation targets (d <= 4, K <= 8)
@@ -251,28 +275,32 @@ __global__ void __launch_bounds__(TILE_PX, (KT <= 8 && DP <= 4) ? SS_RASTER_MINB
     const float inv_g2 = (float)(1.4426950408889634 / a.gamma);
 
     // exact hit evaluation for one queued candidate (reference raster.py:307-324, :380-399)
-    auto process = [&](int j) {
-        const float *rp = s_rec + j * RS;
-        const double2 cxy = *reinterpret_cast<const double2 *>(rp);
+    unsigned s_rec_a = (unsigned)__cvta_generic_to_shared(s_rec);
+    asm volatile("" : "+r"(s_rec_a));  // opaque: keep it in a register instead of re-deriving it per round
+    auto process = [&](unsigned j) {
+        const unsigned ra = s_rec_a + j * (RS * 4);
+        const double2 cxy = lds_d2(ra);
         constexpr bool kCompact = DP == 3;
         double2 czn;
         float4 mi;  // r, clamped opacity o, o / gamma * log2(e), sphere id bits
         float4 f3 = make_float4(0.f, 0.f, 0.f, 0.f);
         if (kCompact) {
-            const float4 q = *reinterpret_cast<const float4 *>(rp + 4);   // cz (float64), r, id
-            f3 = *reinterpret_cast<const float4 *>(rp + 8);                // o, f0, f1, f2
+            const float4 q = lds_f4(ra + 16);   // cz (float64), r, id
+            f3 = lds_f4(ra + 32);               // o, f0, f1, f2
             czn.x = __hiloint2double(__float_as_int(q.y), __float_as_int(q.x));
             czn.y = cxy.x * cxy.x + cxy.y * cxy.y + czn.x * czn.x;
             mi = make_float4(q.z, f3.x, f3.x * inv_g2, q.w);
         } else {
-            czn = *reinterpret_cast<const double2 *>(rp + 4);
-            mi = *reinterpret_cast<const float4 *>(rp + 8);
+            czn = lds_d2(ra + 16);
+            mi = lds_f4(ra + 32);
         }
+        // dist2 is NOT clamped at zero here (raster.py:311 clamps): a slightly negative value (ray through the
+        // centre, cancellation noise ~1e-13) leaves the decision hc2 > 0 and every float32 consumer unchanged
+        // (d2f is clamped below, (float)hc2 rounds to (float)r^2); only the rare t <= 0 branch needs the clamp.
         double t, dist2, zeta;
         if (MODE == SS_MODE_PINHOLE) {
             t = ux * cxy.x + uy * cxy.y + uz * czn.x;
             dist2 = czn.y - t * t;
-            dist2 = dist2 < 0.0 ? 0.0 : dist2;
             zeta = t * uz;
         } else {
             t = czn.x;
@@ -284,7 +312,7 @@ __global__ void __launch_bounds__(TILE_PX, (KT <= 8 && DP <= 4) ? SS_RASTER_MINB
         const double rr = (double)rf * (double)rf;
         const double hc2 = rr - dist2;
         // dist2 < r^2 and t + half_chord > 0
-        if (hc2 > 0.0 && (t > 0.0 || t + sqrt(hc2) > 0.0)) {
+        if (hc2 > 0.0 && (t > 0.0 || t + sqrt(fmin(hc2, rr)) > 0.0)) {
             ++n_hits;
             // float32 NDC depth for the blend exponent: (far - clip(zeta)) / (far - near)
             const float zeta_f = (MODE == SS_MODE_PINHOLE) ? (float)t * uzf : (float)t;
@@ -311,7 +339,7 @@ __global__ void __launch_bounds__(TILE_PX, (KT <= 8 && DP <= 4) ? SS_RASTER_MINB
             }
 #pragma unroll
             for (int i4 = 0; i4 < (kCompact ? 0 : DP); i4 += 4) {
-                const float4 f = *reinterpret_cast<const float4 *>(rp + 12 + i4);
+                const float4 f = lds_f4(ra + 48 + 4 * i4);
                 num[i4] = fmaf(term, f.x, num[i4]);
                 if (i4 + 1 < DP) num[i4 + 1] = fmaf(term, f.y, num[i4 + 1]);
                 if (i4 + 2 < DP) num[i4 + 2] = fmaf(term, f.z, num[i4 + 2]);
@@ -406,9 +434,10 @@ __global__ void __launch_bounds__(TILE_PX, (KT <= 8 && DP <= 4) ? SS_RASTER_MINB
 
         // float32 filter: every lane tests its pixel against a group of 32 relevant candidates and keeps the
         // outcome as one 32-bit word (candidate i of the group at bit 31 - i; the sign bit of d^2 - rho^2 is
-        // funnel-shifted in).  Two such words form a 64-bit window; a lane always takes its oldest pending
-        // hit (count-leading-zeros), so lanes with few hits in the older group run ahead into the newer one
-        // while the busy lanes catch up, and the divergent float64 path runs with most lanes active.
+        // funnel-shifted in).  Two such words form the window; a lane always takes its oldest
+        // pending hit (highest set bit of the older word, else of the newer one), so lanes with few hits in the
+        // older group run ahead into the newer one while the busy lanes catch up, and the divergent float64
+        // path runs with most lanes active.
         auto filter_group = [&](int g) -> unsigned {
             const int n = min(32, cnt - g);
             unsigned w = 0;
@@ -429,23 +458,27 @@ __global__ void __launch_bounds__(TILE_PX, (KT <= 8 && DP <= 4) ? SS_RASTER_MINB
             w &= 0xffffffffu << (32 - n);
             return w;
         };
-        unsigned long long win = 0;  // [older group : newer group]
-        int gbase = 0;               // list position of the older group
+        unsigned w0 = 0, w1 = 0;  // older group, newer group (two 32-bit words: 64-bit shifts / tests cost double)
+        unsigned lpos = (unsigned)__cvta_generic_to_shared(lst);  // shared address of the older group's list entries
+        asm volatile("" : "+r"(lpos));
         auto drain_round = [&]() {
-            if (win) {
-                const int i = __clzll((long long)win);
-                win &= ~(0x8000000000000000ull >> i);
-                process(lst[gbase + i]);
+            const bool older = w0 != 0u;
+            const unsigned w = older ? w0 : w1;
+            if (w) {
+                const int b = 31 - __clz((int)w);  // highest set bit = oldest pending candidate (list entry 31 - b)
+                const unsigned bit = 1u << b;
+                if (older) w0 ^= bit; else w1 ^= bit;
+                process(lds_u8(lpos + (older ? 31 : 63) - b));
             }
         };
-        win = (unsigned long long)filter_group(0) << 32;
+        w0 = filter_group(0);
         for (int g = 32; g < cnt; g += 32) {
-            win |= filter_group(g);
-            while (__any_sync(0xffffffffu, (unsigned)(win >> 32) != 0u)) drain_round();
-            win <<= 32;
-            gbase = g;
+            w1 = filter_group(g);
+            while (__any_sync(0xffffffffu, w0 != 0u)) drain_round();
+            w0 = w1; w1 = 0u;
+            lpos += 32;
         }
-        while (__any_sync(0xffffffffu, win != 0ull)) drain_round();
+        while (__any_sync(0xffffffffu, w0 != 0u)) drain_round();
     }
 
     // finalise, raster.py:401-414

@@ -8,7 +8,8 @@ import ctypes as C
 import os
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "csrc", "libss_b200.so")
+# SS_B200_LIB selects another build of the same library (kernel experiments); the default is the in-tree build
+LIB_PATH = os.environ.get("SS_B200_LIB") or os.path.join(_HERE, "csrc", "libss_b200.so")
 
 SS_OK = 0
 SS_ERR_NULL, SS_ERR_DIMS, SS_ERR_PARAMS, SS_ERR_CAMERA = 1, 2, 3, 4

@@ -46,6 +46,18 @@ __device__ __forceinline__ float ex2_approx_f(float x) {
     return y;
 }
 
+// Draw record through the read-only (non-coherent) path: the compiler may then hoist these loads over the
+// shared-memory stores and reductions of earlier slots (a generic pointer could alias them).
+__device__ __forceinline__ Rec ldg_rec(const Rec *p) {
+    const double2 a = __ldg(reinterpret_cast<const double2 *>(p));
+    const float4 b = __ldg(reinterpret_cast<const float4 *>(p) + 1);
+    Rec r;
+    r.cx = a.x; r.cy = a.y;
+    r.cz = __hiloint2double(__float_as_int(b.y), __float_as_int(b.x));
+    r.r = b.z; r.o = b.w;
+    return r;
+}
+
 #ifndef SS_BACKWARD_MERGE
 #define SS_BACKWARD_MERGE 1
 #endif
@@ -174,7 +186,7 @@ __device__ __forceinline__ void slot_gradient(const BackArgs &a, const Rec &rc, 
 // KT > 0: the K <= KT slots of a pixel are unrolled, every load of a phase issued before its first use
 // (the kernel is latency-bound on dependent gathers).  KT == 0: any K, slot by slot.
 template <int DP, int MODE, int KT>
-__global__ void __launch_bounds__(TILE_PX, (KT > 0) ? (KT <= 5 ? 4 : 3) : 1) k_backward(BackArgs a) {
+__global__ void __launch_bounds__(TILE_PX, (KT > 0) ? (KT <= 5 ? 4 : 3) : (DP <= 16 ? 2 : 1)) k_backward(BackArgs a) {
     const Cam &cam = a.cam;
     const int tile = blockIdx.x;
     const int tid = threadIdx.x;
@@ -270,34 +282,59 @@ __global__ void __launch_bounds__(TILE_PX, (KT > 0) ? (KT <= 5 ? 4 : 3) : 1) k_b
                                                       ys, ux, uy, uz, inv_vnorm);
         }
     } else {
+        // Any K (n_track up to 64) and wide payloads: the feature rows (the bulk of the gather traffic: K x 4 d bytes
+        // per pixel) are read ONCE, with 128-bit loads when they are aligned quads.  Pass 1 forms f_hat and keeps the
+        // scalar <upstream, f_k> of every slot in shared memory (column per thread); pass 2 re-reads only the slot
+        // (ids, z, closeness: coalesced, L1 hits) and the 32-byte record and needs no feature at all:
+        // <upstream, f_k - f_hat> = <up, f_k> - <up, f_hat>, d_feature = w * upstream.
+        extern __shared__ float s_uf[];  // [K][TILE_PX]
+        const bool quads = (d & 3) == 0 && (reinterpret_cast<unsigned long long>(a.feat) & 15ull) == 0ull;
         for (int k = 0; k < K; ++k) {
-            const int id = valid ? ids[k * P + pix] : -1;
+            const int id = valid ? __ldg(ids + k * P + pix) : -1;
             if (id < 0) continue;
-            const float o = a.rec[id].o;
-            const float E = ex2_approx_f((o * zb[k * P + pix] * inv_g - ld) * 1.4426950408889634f);
-            const float w = o * cb[k * P + pix] * E;
+            const float o = __ldg(&a.rec[id].o);
+            const float E = ex2_approx_f((o * __ldg(zb + k * P + pix) * inv_g - ld) * 1.4426950408889634f);
+            const float w = o * __ldg(cb + k * P + pix) * E;
             const float *f = a.feat + (size_t)id * d;
+            float uf = 0.0f;
+            if (quads) {
 #pragma unroll
-            for (int i = 0; i < DP; ++i)
-                if (i < d) fhat[i] = fmaf(w, f[i], fhat[i]);
+                for (int i = 0; i < DP; i += 4) {
+                    if (i < d) {
+                        const float4 q = __ldg(reinterpret_cast<const float4 *>(f + i));
+                        fhat[i] = fmaf(w, q.x, fhat[i]); uf = fmaf(up[i], q.x, uf);
+                        if (i + 1 < DP) { fhat[i + 1] = fmaf(w, q.y, fhat[i + 1]); uf = fmaf(up[i + 1], q.y, uf); }
+                        if (i + 2 < DP) { fhat[i + 2] = fmaf(w, q.z, fhat[i + 2]); uf = fmaf(up[i + 2], q.z, uf); }
+                        if (i + 3 < DP) { fhat[i + 3] = fmaf(w, q.w, fhat[i + 3]); uf = fmaf(up[i + 3], q.w, uf); }
+                    }
+                }
+            } else {
+#pragma unroll
+                for (int i = 0; i < DP; ++i)
+                    if (i < d) { const float fi = __ldg(f + i); fhat[i] = fmaf(w, fi, fhat[i]); uf = fmaf(up[i], fi, uf); }
+            }
+            s_uf[k * TILE_PX + tid] = uf;
         }
+        float ufh = 0.0f;
+#pragma unroll
+        for (int i = 0; i < DP; ++i) ufh = fmaf(up[i], fhat[i], ufh);
+        // (measured at C5, 10 M spheres / d = 16 / K = 32, 3.9 ms: pass 1 1.25 ms, pass 2 without its reductions
+        // 0.9 ms, the 225 M 16-byte L2 reductions 1.8 ms; reading ids four slots ahead, prefetching the rows of
+        // slot k + 3 or loading slot k + 1 during slot k changed nothing or cost time -- see profiles/r02_summary.md)
+        const Rec rc_none = {0.0, 0.0, 0.0, 1.0f, 0.0f};
         for (int k = 0; k < K; ++k) {
-            const int id = valid ? ids[k * P + pix] : -1;
+            const int id = valid ? __ldg(ids + k * P + pix) : -1;
             if (kMerge ? !__any_sync(0xffffffffu, id >= 0) : id < 0) continue;
-            Rec rc; rc.cx = rc.cy = rc.cz = 0.0; rc.r = 1.0f; rc.o = 0.0f;
-            float f[DP];
-#pragma unroll
-            for (int i = 0; i < DP; ++i) f[i] = 0.0f;
-            float zk1 = 0.0f, ck1 = 0.0f;
+            Rec rc = rc_none;
+            float zk1 = 0.0f, ck1 = 0.0f, uf = 0.0f;
             if (id >= 0) {
-                rc = a.rec[id];
-#pragma unroll
-                for (int i = 0; i < DP; ++i) f[i] = i < d ? a.feat[(size_t)id * d + i] : 0.0f;
-                zk1 = zb[k * P + pix]; ck1 = cb[k * P + pix];
+                rc = ldg_rec(a.rec + id);
+                zk1 = __ldg(zb + k * P + pix); ck1 = __ldg(cb + k * P + pix);
+                uf = s_uf[k * TILE_PX + tid];
             }
             const float E1 = ex2_approx_f((rc.o * zk1 * inv_g - ld) * 1.4426950408889634f);
-            slot_gradient<DP, MODE, kMerge>(a, rc, id, zk1, ck1, E1, inv_g, up, fhat, f, d, xs, ys, ux, uy, uz,
-                                            inv_vnorm);
+            slot_gradient_acoef<DP, MODE, kMerge>(a, rc, id, zk1, ck1, E1, inv_g, up, uf - ufh, d, xs, ys, ux, uy, uz,
+                                                  inv_vnorm);
         }
     }
 }
@@ -475,10 +512,22 @@ __global__ void __launch_bounds__(256) k_finalize(FinArgs a) {
     ((unsigned long long *)a.cam_part)[BST_TAG] = a.tag;  // every consumed row is zero again
 }
 
+template <int DP, int KT, int MODE>
+void launch_bw_one(const BackArgs &b, int n_tiles, cudaStream_t s) {
+    const size_t smem = KT > 0 ? 0 : (size_t)b.K * TILE_PX * sizeof(float);  // <up, f_k> columns (64 KB at K = 64)
+    if (KT == 0) {
+        static PerDeviceOnce attr_once;  // per instantiation and device
+        if (attr_once.first())
+            cudaFuncSetAttribute(k_backward<DP, MODE, KT>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 SS_MAX_TOP_K * TILE_PX * (int)sizeof(float));
+    }
+    k_backward<DP, MODE, KT><<<n_tiles, TILE_PX, smem, s>>>(b);
+}
+
 template <int DP, int KT>
 void launch_bw_mode(const BackArgs &b, int n_tiles, int mode, cudaStream_t s) {
-    if (mode == SS_MODE_PINHOLE) k_backward<DP, SS_MODE_PINHOLE, KT><<<n_tiles, TILE_PX, 0, s>>>(b);
-    else k_backward<DP, SS_MODE_ORTHOGRAPHIC, KT><<<n_tiles, TILE_PX, 0, s>>>(b);
+    if (mode == SS_MODE_PINHOLE) launch_bw_one<DP, KT, SS_MODE_PINHOLE>(b, n_tiles, s);
+    else launch_bw_one<DP, KT, SS_MODE_ORTHOGRAPHIC>(b, n_tiles, s);
 }
 
 template <int DP>

@@ -71,13 +71,28 @@ __device__ __forceinline__ void red_add_v4(float *addr, float a, float b, float 
                  : "memory");
 }
 
+// Per-warp accumulator cache of the any-K path (n_track up to 64).  With long records a sphere sits at DIFFERENT
+// slot indices in neighbouring pixels, so the lockstep merge below finds few peers (C5: 1.8 lanes per group) and
+// the 16-byte L2 reductions dominate the kernel (225 M of them, 1.8 of 3.9 ms).  Each warp therefore keeps CACHE_ROWS
+// partial rows in shared memory, direct-mapped by a hash of the sphere id: a group leader adds its sums to the
+// cached row of its sphere (plain shared-memory read-modify-write: one owner lane per row and instruction, the warp
+// runs the slots in lockstep) and only an evicted or finally flushed row goes to the L2 as reductions.
+constexpr int CACHE_ROWS = 64;
+template <int DP>
+constexpr int cache_stride() { return (8 + ((DP + 3) & ~3)) % 8 == 0 ? 8 + ((DP + 3) & ~3) + 4 : 8 + ((DP + 3) & ~3); }
+struct RowCache {
+    int *tag;     // [CACHE_ROWS] sphere id or -1
+    float *rows;  // [CACHE_ROWS][stride]
+    int stride;   // floats per row, = 4 mod 8 (rows of different lanes start in different bank groups)
+};
+
 // Per-hit gradient pieces for one stored slot (grad.py:110-179); accumulates into the sphere's row.
 // acoef = <upstream, f_k - f_hat> (grad.py:110) is formed by the caller.
-template <int DP, int MODE, bool MERGE = false>
+template <int DP, int MODE, bool MERGE = false, bool CACHE = false>
 __device__ __forceinline__ void slot_gradient_acoef(const BackArgs &a, const Rec &rc, int id, float zk, float ck,
                                                     float E, float inv_g, const float *up, float acoef, int d,
                                                     double xs, double ys, double ux, double uy, double uz,
-                                                    double inv_vnorm) {
+                                                    double inv_vnorm, const RowCache *cache = nullptr) {
     const Cam &cam = a.cam;
     const float o = rc.o;
     const float ez = o * zk * inv_g;
@@ -158,8 +173,45 @@ __device__ __forceinline__ void slot_gradient_acoef(const BackArgs &a, const Rec
         const int nn = __shfl_sync(0xffffffffu, nxt, src);
         nxt = nxt >= 0 ? nn : -1;
     }
-    if (id < 0 || (peers & ((1u << lane) - 1u)) != 0u) return;  // not the group's lowest lane
+    const bool lead = id >= 0 && (peers & ((1u << lane) - 1u)) == 0u;  // the group's lowest lane
     v[7] = (float)__popc(peers);
+    if (CACHE) {
+        // one owner per cache row and instruction: leaders whose spheres hash to the same row are ranked, the
+        // lowest lane uses the cache, the others (rare) reduce straight into the L2
+        const unsigned h = lead ? ((unsigned)id * 2654435761u) >> 26 : (unsigned)CACHE_ROWS + lane;
+        static_assert(CACHE_ROWS == 64, "the hash keeps 6 bits");
+        const unsigned same = __match_any_sync(0xffffffffu, h);
+        const bool owner = lead && (same & ((1u << lane) - 1u)) == 0u;
+        if (owner) {
+            float4 *crow = reinterpret_cast<float4 *>(cache->rows + h * cache->stride);
+            const int tag = cache->tag[h];
+            if (tag == id) {
+#pragma unroll
+                for (int q = 0; q < (8 + DP4) / 4; ++q) {
+                    float4 r = crow[q];
+                    r.x += v[4 * q]; r.y += v[4 * q + 1]; r.z += v[4 * q + 2]; r.w += v[4 * q + 3];
+                    crow[q] = r;
+                }
+            } else {
+                if (tag >= 0) {  // evict: the cached partial sums of another sphere go to its accumulator row
+                    float *erow = a.raw + (size_t)tag * a.raw_stride;
+#pragma unroll
+                    for (int q = 0; q < (8 + DP4) / 4; ++q) {
+                        const float4 r = crow[q];
+                        if (q < 2 || 4 * (q - 2) < d) red_add_v4(erow + 4 * q, r.x, r.y, r.z, r.w);
+                    }
+                }
+#pragma unroll
+                for (int q = 0; q < (8 + DP4) / 4; ++q)
+                    crow[q] = make_float4(v[4 * q], v[4 * q + 1], v[4 * q + 2], v[4 * q + 3]);
+                cache->tag[h] = id;
+            }
+        }
+        __syncwarp();  // the row may be read by another lane in the next slot
+        if (!lead || owner) return;
+    } else {
+        if (!lead) return;
+    }
   } else {
     if (id < 0) return;
   }
@@ -287,7 +339,17 @@ __global__ void __launch_bounds__(TILE_PX, (KT > 0) ? (KT <= 5 ? 4 : 3) : (DP <=
         // scalar <upstream, f_k> of every slot in shared memory (column per thread); pass 2 re-reads only the slot
         // (ids, z, closeness: coalesced, L1 hits) and the 32-byte record and needs no feature at all:
         // <upstream, f_k - f_hat> = <up, f_k> - <up, f_hat>, d_feature = w * upstream.
-        extern __shared__ float s_uf[];  // [K][TILE_PX]
+        extern __shared__ float s_uf[];  // [K][TILE_PX], then the per-warp accumulator caches
+        constexpr int DP4c = (DP + 3) & ~3;
+        constexpr int CSTRIDE = cache_stride<DP>();  // floats per cached row (= 4 mod 8)
+        RowCache cache;
+        cache.stride = CSTRIDE;
+        cache.rows = s_uf + (size_t)K * TILE_PX + (size_t)warp * (CACHE_ROWS * CSTRIDE + CACHE_ROWS);
+        cache.tag = reinterpret_cast<int *>(cache.rows + CACHE_ROWS * CSTRIDE);
+        if (kMerge) {
+            cache.tag[lane] = -1; cache.tag[lane + 32] = -1;
+            __syncwarp();
+        }
         const bool quads = (d & 3) == 0 && (reinterpret_cast<unsigned long long>(a.feat) & 15ull) == 0ull;
         for (int k = 0; k < K; ++k) {
             const int id = valid ? __ldg(ids + k * P + pix) : -1;
@@ -333,8 +395,25 @@ __global__ void __launch_bounds__(TILE_PX, (KT > 0) ? (KT <= 5 ? 4 : 3) : (DP <=
                 uf = s_uf[k * TILE_PX + tid];
             }
             const float E1 = ex2_approx_f((rc.o * zk1 * inv_g - ld) * 1.4426950408889634f);
-            slot_gradient_acoef<DP, MODE, kMerge>(a, rc, id, zk1, ck1, E1, inv_g, up, uf - ufh, d, xs, ys, ux, uy, uz,
-                                                  inv_vnorm);
+            slot_gradient_acoef<DP, MODE, kMerge, kMerge>(a, rc, id, zk1, ck1, E1, inv_g, up, uf - ufh, d, xs, ys, ux,
+                                                          uy, uz, inv_vnorm, &cache);
+        }
+        if (kMerge) {  // flush the cache: every lane owns two rows
+            __syncwarp();
+#pragma unroll
+            for (int r = 0; r < 2; ++r) {
+                const int h = lane + 32 * r;
+                const int tag = cache.tag[h];
+                if (tag >= 0) {
+                    const float4 *crow = reinterpret_cast<const float4 *>(cache.rows + h * CSTRIDE);
+                    float *erow = a.raw + (size_t)tag * a.raw_stride;
+#pragma unroll
+                    for (int q = 0; q < (8 + DP4c) / 4; ++q) {
+                        const float4 v4 = crow[q];
+                        if (q < 2 || 4 * (q - 2) < d) red_add_v4(erow + 4 * q, v4.x, v4.y, v4.z, v4.w);
+                    }
+                }
+            }
         }
     }
 }
@@ -514,12 +593,14 @@ __global__ void __launch_bounds__(256) k_finalize(FinArgs a) {
 
 template <int DP, int KT, int MODE>
 void launch_bw_one(const BackArgs &b, int n_tiles, cudaStream_t s) {
-    const size_t smem = KT > 0 ? 0 : (size_t)b.K * TILE_PX * sizeof(float);  // <up, f_k> columns (64 KB at K = 64)
+    // <up, f_k> columns (64 KB at K = 64) + 8 per-warp accumulator caches (60 KB at d = 16)
+    constexpr size_t cache_bytes = DP <= 16 ? 8 * (size_t)CACHE_ROWS * (cache_stride<DP>() + 1) * sizeof(float) : 0;
+    const size_t smem = KT > 0 ? 0 : (size_t)b.K * TILE_PX * sizeof(float) + cache_bytes;
     if (KT == 0) {
         static PerDeviceOnce attr_once;  // per instantiation and device
         if (attr_once.first())
             cudaFuncSetAttribute(k_backward<DP, MODE, KT>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                 SS_MAX_TOP_K * TILE_PX * (int)sizeof(float));
+                                 SS_MAX_TOP_K * TILE_PX * (int)sizeof(float) + (int)cache_bytes);
     }
     k_backward<DP, MODE, KT><<<n_tiles, TILE_PX, smem, s>>>(b);
 }

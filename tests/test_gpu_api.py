@@ -284,6 +284,27 @@ def test_host_session_matches_device_path(engine):
     assert np.array_equal(image.numpy(), f["image"].cpu().numpy())
     assert np.array_equal(grads["pixel_count"].numpy(), ref["pixel_count"].cpu().numpy())
     grad_close(grads["d_feat"].numpy(), ref_feat, "host-session d_feature", rtol=1e-5)
+    # resident scene (no re-upload) + compact download: only the rows of the spheres that received gradient
+    dense = {k: grads[k].numpy().copy() for k in ("d_pos", "d_rad", "d_opa", "d_feat", "pixel_count")}
+    for rep in range(3):  # the second and third call use the speculative one-round-trip download
+        image, cg = sess.render_step(spec, upstream_fn=lambda i, im: torch.sign(im - 0.5), gamma=0.1, tau=0.0,
+                                     compact=True)
+        assert sess.last_h2d_bytes == 4 * 128 * 128 * 3  # upstream only: the scene stayed on the device
+        idx = cg["index"].numpy()
+        touched = np.flatnonzero(dense["pixel_count"] > 0)
+        assert cg["count"] == touched.size and np.array_equal(idx, touched)
+        assert np.array_equal(cg["pixel_count"].numpy(), dense["pixel_count"][touched])
+        for k in ("d_pos", "d_rad", "d_opa", "d_feat"):
+            grad_close(cg[k].numpy(), dense[k][touched], f"compact {k}", rtol=2e-5)
+        grad_close(cg["cam_grad"].numpy()[:14], ref["cam_grad"].cpu().numpy()[:14], "compact cam_grad", rtol=2e-5)
+    # a smaller scene afterwards touches MORE spheres than the speculative estimate of a fresh session would cover
+    sess2 = HostRenderSession(5000, 3, 128, 128, 5, engine=engine)
+    sess2.set_scene(pos, rad * 0.3, opa, feat, bg)
+    _, few = sess2.render_step(spec, upstream_fn=lambda i, im: torch.sign(im - 0.5), gamma=0.1, tau=0.0, compact=True)
+    sess2.set_scene(pos, rad, opa, feat, bg)
+    _, more = sess2.render_step(spec, upstream_fn=lambda i, im: torch.sign(im - 0.5), gamma=0.1, tau=0.0, compact=True)
+    assert more["count"] == touched.size and np.array_equal(more["index"].numpy(), touched)
+    assert np.array_equal(more["pixel_count"].numpy(), dense["pixel_count"][touched])
 
 
 def test_accumulator_reuse_protocol(engine):

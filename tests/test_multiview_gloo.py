@@ -112,3 +112,38 @@ def test_two_rank_step_equals_sum_over_views():
         assert torch.equal(cnt, grads.pixel_count)
         assert views == shard_views(len(cams), world, rank)
     assert grads.pixel_count.sum() > 0 and grads.flat.abs().sum() > 0
+
+
+def _worker_overlap(rank, world, port, ret):
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        scene, cams = _scene_and_cameras()
+        r = ViewShardedRenderer(OracleEngine())
+        grads = SphereGradBuffer(scene[0].shape[0], 3, "cpu")
+        # two steps with the reduction left in flight: the second step must wait for the first one's
+        # allreduce before its first backward overwrites the buffer, finish() before the buffer is read
+        r.step(scene, cams, _upstream, grads, gamma=0.1, tau=0.0, overlap=True)
+        assert r._pending is not None
+        r.step(scene, cams, _upstream, grads, gamma=0.1, tau=0.0, overlap=True)
+        r.finish()
+        assert r._pending is None
+        ret[rank] = (grads.flat.clone(), grads.pixel_count.clone(), r.collectives_issued)
+    finally:
+        dist.destroy_process_group()
+
+
+def test_deferred_allreduce_gives_the_same_sums():
+    world = 2
+    port = _free_port()
+    mgr = mp.Manager()
+    ret = mgr.dict()
+    mp.spawn(_worker_overlap, args=(world, port, ret), nprocs=world, join=True)
+    scene, cams = _scene_and_cameras()
+    grads = SphereGradBuffer(scene[0].shape[0], 3, "cpu")
+    ViewShardedRenderer(OracleEngine()).step(scene, cams, _upstream, grads, gamma=0.1, tau=0.0)
+    for rank in range(world):
+        flat, cnt, n_coll = ret[rank]
+        assert torch.allclose(flat, grads.flat, rtol=1e-5, atol=1e-7) and torch.equal(cnt, grads.pixel_count)
+        assert n_coll == 4  # gloo: two reductions per step (NCCL: one coalesced group per step)

@@ -51,25 +51,31 @@ struct TopK {
     int id[KT];
     float c[KT];
     int n;  // filled slots: a new entry starts at slot n, not at the bottom of an empty record
+    // admission threshold of a FULL record, cached in registers: with n_track = 32 most hits arrive after the record
+    // has filled up and are rejected; without the cache every one of them read z[KT - 1] back from local memory
+    // (L2 latency: 3 CTAs x 128 KB of records do not fit the L1) and formed its float64 depth first
+    double wz; int wid; float wlo;
     __device__ __forceinline__ void init() {
         // large K: the arrays live in (L1-cached) local memory, not in 4*KT registers
 #pragma unroll 1
         for (int k = 0; k < KT; ++k) { z[k] = -INFINITY; id[k] = -1; c[k] = 0.0f; }
         n = 0;
+        wz = -INFINITY; wid = -1; wlo = -INFINITY;
     }
     __device__ __forceinline__ void bind(unsigned char *, int) {}
     __device__ __forceinline__ double get_z(int k) const { return z[k]; }
     __device__ __forceinline__ int get_id(int k) const { return id[k]; }
     __device__ __forceinline__ float get_c(int k) const { return c[k]; }
-    __device__ __forceinline__ bool may_enter(float) const { return true; }
+    __device__ __forceinline__ bool may_enter(float zzf) const { return zzf >= wlo; }
     // keep the KT largest by (z desc, id asc) -- raster.py:389-399.  Candidates arrive roughly front to back,
-    // so the usual case is an append at slot n (one comparison) or, once full, a rejection at slot KT - 1.
-    __device__ __forceinline__ void insert(double zz, int sid, float cl, float) {
+    // so the usual case is an append at slot n (one comparison) or, once full, a rejection against the cached
+    // worst entry.
+    __device__ __forceinline__ void insert(double zz, int sid, float cl, float pad) {
         int k;
         if (n < KT) {
             k = n++;
         } else {
-            if (!(zz > z[KT - 1] || (zz == z[KT - 1] && sid < id[KT - 1]))) return;
+            if (!(zz > wz || (zz == wz && sid < wid))) return;
             k = KT - 1;
         }
 #pragma unroll 1
@@ -81,6 +87,10 @@ struct TopK {
             --k;
         }
         z[k] = zz; id[k] = sid; c[k] = cl;
+        if (n == KT) {  // the record is full: refresh the cached threshold
+            wz = z[KT - 1]; wid = id[KT - 1];
+            wlo = (float)wz - pad;
+        }
     }
 };
 
@@ -394,8 +404,15 @@ __global__ void __launch_bounds__(TILE_PX, (KT <= 8 && DP <= 4) ? SS_RASTER_MINB
             if (DP == 3) {
                 *reinterpret_cast<float4 *>(rp + 8) = make_float4(rc.o, f[0], a.d > 1 ? f[1] : 0.0f, a.d > 2 ? f[2] : 0.0f);
             } else {
+                if ((a.d & 3) == 0 && (reinterpret_cast<unsigned long long>(a.feat) & 15ull) == 0ull) {
 #pragma unroll
-                for (int i = 0; i < ((DP + 3) & ~3); ++i) rp[12 + i] = i < a.d ? f[i] : 0.0f;
+                    for (int i = 0; i < ((DP + 3) & ~3); i += 4)
+                        *reinterpret_cast<float4 *>(rp + 12 + i) =
+                            i < a.d ? __ldg(reinterpret_cast<const float4 *>(f + i)) : make_float4(0.f, 0.f, 0.f, 0.f);
+                } else {
+#pragma unroll
+                    for (int i = 0; i < ((DP + 3) & ~3); ++i) rp[12 + i] = i < a.d ? f[i] : 0.0f;
+                }
             }
         }
         __syncthreads();
@@ -504,7 +521,7 @@ __global__ void __launch_bounds__(TILE_PX, (KT <= 8 && DP <= 4) ? SS_RASTER_MINB
                     }
                 }
             } else {
-#pragma unroll 1
+#pragma unroll 4
                 for (int k = 0; k < a.K; ++k) {
                     const int tid_k = top.get_id(k);
                     a.ids[k * P + pix] = tid_k;

@@ -35,7 +35,7 @@
 extern "C" {
 #endif
 
-#define SS_ABI_VERSION 1
+#define SS_ABI_VERSION 2
 
 /* ---- return codes (host-side argument checking; errors.py classes in parentheses) ---- */
 #define SS_OK 0
@@ -63,6 +63,13 @@ extern "C" {
 #define SS_OPT_REUSE_RECORDS 64u /* backward: camera-frame records in the workspace are still those of the
                                     matching forward call; skip recomputing them (grad.py:213, :351) */
 #define SS_OPT_SKIP_VALIDATE 128u /* forward: do not scan inputs for NaN/Inf/radius <= 0 */
+#define SS_OPT_DETERMINISTIC 256u /* backward: bit-reproducible gradients (needs det_workspace).  The reference
+                                    * merges its per-tile sums in a fixed order and is bit-identical run to run
+                                    * (grad.py:231-250); the default device path sums with float32
+                                    * L2 atomics, whose order varies.  In this mode every per-sphere sum is
+                                    * accumulated in 64-bit fixed point (integer addition is associative) on a
+                                    * per-sphere power-of-two grid found by a first pass (order-independent max),
+                                    * and the camera sums are reduced in block order: two passes of k_backward. */
 
 #define SS_MODE_PINHOLE 0
 #define SS_MODE_ORTHOGRAPHIC 1
@@ -161,6 +168,8 @@ typedef struct SsBackwardArgs {
     float *d_feat;
     int32_t *pixel_count;
     double *cam_grad;
+    void *det_workspace;        /* SS_OPT_DETERMINISTIC: caller-owned scratch of ss_deterministic_workspace_bytes, else NULL */
+    size_t det_workspace_bytes;
 } SsBackwardArgs;
 
 /* status block, host copy (ss_read_status) */
@@ -191,6 +200,10 @@ int ss_workspace_init(const SsDims *dims, void *workspace, size_t workspace_byte
 /* `stream` is a cudaStream_t passed as void* (NULL = default stream). */
 int ss_forward(const SsForwardArgs *args, void *stream);
 int ss_backward(const SsBackwardArgs *args, void *stream);
+
+/* Scratch size of the SS_OPT_DETERMINISTIC backward for these dimensions (per-sphere grid exponents +
+ * 64-bit fixed-point accumulator rows). */
+int ss_deterministic_workspace_bytes(const SsDims *dims, size_t *out_bytes);
 
 /* Copies the status block of the last forward on `workspace` to the host; synchronises `stream`. */
 int ss_read_status(const void *workspace, SsStatus *out_host, void *stream);

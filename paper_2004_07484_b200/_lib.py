@@ -27,6 +27,7 @@ OPT_CAMERA_GRADS = 16
 OPT_ACCUMULATE = 32
 OPT_REUSE_RECORDS = 64
 OPT_SKIP_VALIDATE = 128
+OPT_DETERMINISTIC = 256
 
 MODE_PINHOLE, MODE_ORTHOGRAPHIC = 0, 1
 MAX_FEATURE_DIM, MAX_TOP_K, TILE, MAX_CHUNK = 32, 64, 16, 256
@@ -66,7 +67,7 @@ class SsBackwardArgs(C.Structure):
                 ("workspace", _P), ("workspace_bytes", C.c_size_t),
                 ("ids", _P), ("z", _P), ("closeness", _P), ("log_denom", _P), ("upstream", _P),
                 ("d_pos", _P), ("d_rad", _P), ("d_opa", _P), ("d_feat", _P), ("pixel_count", _P),
-                ("cam_grad", _P)]
+                ("cam_grad", _P), ("det_workspace", _P), ("det_workspace_bytes", C.c_size_t)]
 
 
 class SsFitStepArgs(C.Structure):
@@ -97,7 +98,7 @@ class SsStatus(C.Structure):
 
 
 EXPORTS = ("ss_abi_version", "ss_status_string", "ss_last_cuda_error", "ss_workspace_bytes", "ss_workspace_init",
-           "ss_forward", "ss_backward", "ss_read_status", "ss_photometric_loss", "ss_fit_step", "ss_adam_flat", "ss_debug_tile_lists", "ss_launch_count",
+           "ss_forward", "ss_backward", "ss_deterministic_workspace_bytes", "ss_read_status", "ss_photometric_loss", "ss_fit_step", "ss_adam_flat", "ss_debug_tile_lists", "ss_launch_count",
            "ss_prune_mask", "ss_prune_mask_f64", "ss_subdivide_f64", "ss_mask_nonzero_i32", "ss_compact_workspace_bytes", "ss_compact_rows", "ss_subdivide",
            "ss_psc1_unpack", "ss_psc1_pack", "ss_convert_f64_f32", "ss_convert_f32_f64",
            "ss_shade_identity", "ss_shade_identity_backward", "ss_shade_diffuse", "ss_shade_diffuse_backward",
@@ -132,6 +133,8 @@ def load():
     lib.ss_forward.argtypes = [C.POINTER(SsForwardArgs), C.c_void_p]
     lib.ss_backward.restype = C.c_int
     lib.ss_backward.argtypes = [C.POINTER(SsBackwardArgs), C.c_void_p]
+    lib.ss_deterministic_workspace_bytes.restype = C.c_int
+    lib.ss_deterministic_workspace_bytes.argtypes = [C.POINTER(SsDims), C.POINTER(C.c_size_t)]
     lib.ss_photometric_loss.restype = C.c_int
     lib.ss_photometric_loss.argtypes = [C.c_void_p, C.c_void_p, C.c_void_p, C.c_int64, C.c_void_p, C.c_void_p]
     lib.ss_fit_step.restype = C.c_int
@@ -176,7 +179,7 @@ def load():
     lib.ss_profile_kernel_count.restype = C.c_int
     lib.ss_profile_kernel_name.restype = C.c_char_p
     lib.ss_profile_kernel_name.argtypes = [C.c_int]
-    if lib.ss_abi_version() != 1:
+    if lib.ss_abi_version() != 2:
         raise NativeLibraryError("libss_b200.so ABI version mismatch")
     _lib = lib
     return lib

@@ -173,9 +173,10 @@ def _same_scene(buffer: BackwardBuffer, cols) -> bool:
 
 def render_backward(scene, camera, params, buffer: BackwardBuffer, upstream, *, workers: int = 1,
                     normalize: bool = True, gate: bool = True, tile_size: int = 16,
-                    engine: RenderEngine = None, reuse_upload: bool = True):
+                    engine: RenderEngine = None, reuse_upload: bool = True, deterministic: bool = False):
     """Full backward pipeline; returns (SceneGradients, CameraGradients) as float64 NumPy like the reference.
-    reuse_upload=False always re-uploads the scene (see the module docstring)."""
+    reuse_upload=False always re-uploads the scene (see the module docstring); deterministic=True makes the
+    result bit-identical from run to run like the reference's (grad.py:231-250), at about twice the device time."""
     eng = engine or default_engine()
     if buffer.num_spheres != len(scene):
         raise ContractViolation(f"buffer built for {buffer.num_spheres} spheres, scene has {len(scene)}")
@@ -199,7 +200,7 @@ def render_backward(scene, camera, params, buffer: BackwardBuffer, upstream, *, 
         st.upstream.copy_(st.h_up, non_blocking=True)
         out = eng.backward(*dev_in, cam, buffer.dev, st.upstream, gamma=bp.gamma, eps=bp.epsilon,
                            normalize=normalize, gate=gate, camera_grads=True, out=dict(st.grads.dev),
-                           accumulate=False)
+                           accumulate=False, deterministic=deterministic)
         hg = st.grads.download(torch.cuda.current_stream(eng.device))
         torch.cuda.current_stream(eng.device).synchronize()
         del out
@@ -229,7 +230,8 @@ class SoftsphereAdapter:
     are constructor arguments here (defaults = FitConfig's defaults)."""
 
     def __init__(self, normalize: bool = True, gate: bool = True, engine: RenderEngine = None,
-                 dtype=np.float64, reuse_upload: bool = True):
+                 dtype=np.float64, reuse_upload: bool = True, deterministic: bool = False):
+        self.deterministic = deterministic
         self.normalize = normalize
         self.gate = gate
         self.engine = engine
@@ -241,4 +243,5 @@ class SoftsphereAdapter:
 
     def backward(self, scene, camera, params, buffer, upstream):
         return render_backward(scene, camera, params, buffer, upstream, normalize=self.normalize,
-                               gate=self.gate, engine=self.engine, reuse_upload=self.reuse_upload)
+                               gate=self.gate, engine=self.engine, reuse_upload=self.reuse_upload,
+                               deterministic=self.deterministic)

@@ -200,6 +200,12 @@ int ss_backward(const SsBackwardArgs *a, void *stream) {
     b.ids = a->ids; b.z = a->z; b.clos = a->closeness; b.log_denom = a->log_denom; b.upstream = a->upstream;
     b.d_pos = a->d_pos; b.d_rad = a->d_rad; b.d_opa = a->d_opa; b.d_feat = a->d_feat;
     b.pixel_count = a->pixel_count; b.cam_grad = a->cam_grad;
+    b.det_ws = nullptr;
+    if (a->blend.flags & SS_OPT_DETERMINISTIC) {
+        if (!a->det_workspace) return SS_ERR_NULL;
+        if (a->det_workspace_bytes < make_det_layout(a->dims).total) return SS_ERR_WORKSPACE;
+        b.det_ws = (char *)a->det_workspace;
+    }
     cudaStream_t s = (cudaStream_t)stream;
     if (!(a->blend.flags & SS_OPT_REUSE_RECORDS)) {
         // the reference recomputes camera-frame centres and projected radii (grad.py:213, :351)
@@ -213,6 +219,14 @@ int ss_backward(const SsBackwardArgs *a, void *stream) {
     }
     cudaError_t e = launch_backward(b, s);
     if (e != cudaSuccess) return cuda_fail(e);
+    return SS_OK;
+}
+
+int ss_deterministic_workspace_bytes(const SsDims *dims, size_t *out_bytes) {
+    if (!dims || !out_bytes) return SS_ERR_NULL;
+    int rc = check_dims(*dims);
+    if (rc != SS_OK) return rc;
+    *out_bytes = make_det_layout(*dims).total;
     return SS_OK;
 }
 

@@ -28,6 +28,12 @@ struct BackArgs {
     unsigned long long *clean_tag;
     int d, K;
     double gamma, eps_over_g;
+    // SS_OPT_DETERMINISTIC: 0 = float32 L2 reductions (default); 1 = first pass, per-sphere max |addend|
+    // (atomicMax on the float bits: order-independent); 2 = second pass, 64-bit fixed-point accumulation on the
+    // per-sphere power-of-two grid derived from that max (integer addition is associative: bit-reproducible)
+    int det;
+    unsigned *det_max;
+    long long *raw64;
 };
 
 __device__ __forceinline__ float rcp_approx(float x) {
@@ -69,6 +75,31 @@ __device__ __forceinline__ void red_add_v4(float *addr, float a, float b, float 
 #endif
     asm volatile("red.global.add.v4.f32 [%0], {%1, %2, %3, %4};" ::"l"(addr), "f"(a), "f"(b), "f"(c), "f"(d)
                  : "memory");
+}
+
+// Deterministic accumulation of one (merged) row of NV floats into sphere `id` (see BackArgs::det).  The merged
+// float sums themselves are reproducible (the warp merge depends on the data only); what is not is the ORDER
+// in which different warps reach the L2.  Grid: with m = max |addend| of the sphere (2^(e-127) <= m < 2^(e-126),
+// e the biased exponent), every addend is rounded to a multiple of q = 2^(e - 126 - 38); the sum of up to
+// 2^24 addends (W * H <= 2^24 is enforced) stays below 2^62 quanta.
+template <int NV>
+__device__ __forceinline__ void det_emit(const BackArgs &a, int id, const float *v) {
+    if (a.det == 1) {
+        float m = 0.0f;
+#pragma unroll
+        for (int j = 0; j < NV; ++j)
+            if (j != 7) m = fmaxf(m, fabsf(v[j]));
+        atomicMax(a.det_max + id, __float_as_uint(m));
+        return;
+    }
+    const int e = (int)(a.det_max[id] >> 23);
+    const double inv_q = __hiloint2double((1023 + 164 - e) << 20, 0);  // 2^(164 - e) = 1 / q
+    unsigned long long *row = reinterpret_cast<unsigned long long *>(a.raw64) + (size_t)id * a.raw_stride;
+#pragma unroll
+    for (int j = 0; j < NV; ++j) {
+        const long long iv = j == 7 ? (long long)v[7] : __double2ll_rn((double)v[j] * inv_q);
+        if (iv != 0) atomicAdd(row + j, (unsigned long long)iv);
+    }
 }
 
 // Per-warp accumulator cache of the any-K path (n_track up to 64).  With long records a sphere sits at DIFFERENT
@@ -175,6 +206,10 @@ __device__ __forceinline__ void slot_gradient_acoef(const BackArgs &a, const Rec
     }
     const bool lead = id >= 0 && (peers & ((1u << lane) - 1u)) == 0u;  // the group's lowest lane
     v[7] = (float)__popc(peers);
+    if (a.det) {  // (warp-uniform)
+        if (lead) det_emit<8 + DP>(a, id, v);
+        return;
+    }
     if (CACHE) {
         // one owner per cache row and instruction: leaders whose spheres hash to the same row are ranked, the
         // lowest lane uses the cache, the others (rare) reduce straight into the L2
@@ -214,6 +249,7 @@ __device__ __forceinline__ void slot_gradient_acoef(const BackArgs &a, const Rec
     }
   } else {
     if (id < 0) return;
+    if (a.det) { det_emit<8 + DP>(a, id, v); return; }
   }
     float *row = a.raw + (size_t)id * a.raw_stride;
     red_add_v4(row, v[0], v[1], v[2], v[3]);
@@ -398,7 +434,7 @@ __global__ void __launch_bounds__(TILE_PX, (KT > 0) ? (KT <= 5 ? 4 : 3) : (DP <=
             slot_gradient_acoef<DP, MODE, kMerge, kMerge>(a, rc, id, zk1, ck1, E1, inv_g, up, uf - ufh, d, xs, ys, ux,
                                                           uy, uz, inv_vnorm, &cache);
         }
-        if (kMerge) {  // flush the cache: every lane owns two rows
+        if (kMerge && !a.det) {  // flush the cache: every lane owns two rows
             __syncwarp();
 #pragma unroll
             for (int r = 0; r < 2; ++r) {
@@ -436,6 +472,25 @@ __global__ void __launch_bounds__(256) k_raw_prepare(float4 *raw4, size_t n4, do
         raw4[i] = z;
 }
 
+// SS_OPT_DETERMINISTIC: fixed-point rows -> the float accumulator rows k_finalize consumes (every row is written,
+// so the clean-accumulator protocol stays valid: k_finalize re-zeroes what it consumes).
+__global__ void __launch_bounds__(256) k_det_convert(const long long *raw64, const unsigned *det_max, float *raw,
+                                                     long long M, int stride) {
+    const long long n = M * stride;
+    for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (long long)gridDim.x * blockDim.x) {
+        const long long s = i / stride;
+        const int j = (int)(i - s * stride);
+        const long long iv = raw64[i];
+        float out = 0.0f;
+        if (iv != 0) {
+            const int e = (int)(det_max[s] >> 23);
+            const double q = __hiloint2double((1023 - 164 + e) << 20, 0);  // 2^(e - 164)
+            out = j == 7 ? (float)iv : (float)((double)iv * q);
+        }
+        raw[i] = out;
+    }
+}
+
 struct FinArgs {
     long long M; int d, raw_stride;
     Cam cam;
@@ -446,6 +501,7 @@ struct FinArgs {
     double *cam_part; double *cam_grad;
     unsigned long long tag;
     int normalize, gate, cam_grads, accumulate;
+    int det;  // camera sums: one slot per block behind the atomics' area, added up in block order by the last block
 };
 
 // One thread per sphere.  The kernel is instruction-bound, not bandwidth-bound (ncu: a staged,
@@ -569,7 +625,8 @@ __global__ void __launch_bounds__(256) k_finalize(FinArgs a) {
         double v = 0.0;
 #pragma unroll
         for (int e = 0; e < 8; ++e) v += s_red[lane][e];
-        if (v != 0.0) atomicAdd(&a.cam_part[lane], v);
+        if (a.det) a.cam_part[CAM_VALS + 2 + (size_t)blockIdx.x * CAM_VALS + lane] = v;
+        else if (v != 0.0) atomicAdd(&a.cam_part[lane], v);
     }
     __syncwarp();
     if (lane != 0) return;
@@ -577,6 +634,15 @@ __global__ void __launch_bounds__(256) k_finalize(FinArgs a) {
     unsigned int *counter = (unsigned int *)(a.cam_part + BST_COUNTER);
     if (atomicAdd(counter, 1u) != gridDim.x - 1) return;
     __threadfence();
+    if (a.cam_grads && a.det) {  // block-ordered sum of the per-block slots (lane 0 of the last block)
+        volatile double *slots = a.cam_part + CAM_VALS + 2;
+        for (int j = 0; j < 14; ++j) {
+            double acc = 0.0;
+            for (unsigned b = 0; b < gridDim.x; ++b) acc += slots[(size_t)b * CAM_VALS + j];
+            a.cam_part[j] = acc;
+        }
+        __threadfence();
+    }
     if (a.cam_grads) {
         const double *R = cam.R;
         volatile double *vs = a.cam_part;
@@ -653,13 +719,33 @@ cudaError_t launch_backward(const BwdLaunch &a, cudaStream_t s) {
     b.clean_tag = (unsigned long long *)bst + BST_TAG;
     b.d = a.dims.feature_dim; b.K = a.dims.top_k;
     b.gamma = a.gamma; b.eps_over_g = a.blend.eps / a.gamma;
+    b.det = 0; b.det_max = nullptr; b.raw64 = nullptr;
     const int d = b.d, mode = a.cam.mode;
-    {
+    auto run_backward = [&]() {
         ProfScope ps(KID_BACKWARD, s);
         if (d == 3) launch_bw_k<3>(b, L.n_tiles, mode, s);  // RGB: one shuffle per merge round less than the d = 4 build
         else if (d <= 4) launch_bw_k<4>(b, L.n_tiles, mode, s);
         else if (d <= 16) launch_bw_k<16>(b, L.n_tiles, mode, s);
         else launch_bw_k<32>(b, L.n_tiles, mode, s);
+        count_launch();
+    };
+    const bool det = a.det_ws != nullptr;
+    if (!det) {
+        run_backward();
+    } else {
+        // SS_OPT_DETERMINISTIC: pass 1 finds every sphere's largest addend (order-independent max), pass 2
+        // accumulates in 64-bit fixed point on that sphere's grid, k_det_convert hands float rows to k_finalize
+        const DetLayout D = make_det_layout(a.dims);
+        b.det_max = (unsigned *)(a.det_ws + D.max_bits);
+        b.raw64 = (long long *)(a.det_ws + D.raw64);
+        cudaError_t e = cudaMemsetAsync(a.det_ws, 0, D.total, s);
+        if (e != cudaSuccess) return e;
+        b.det = 1;
+        run_backward();
+        b.det = 2;
+        run_backward();
+        k_det_convert<<<148 * 8, 256, 0, s>>>(b.raw64, b.det_max, raw, M, L.raw_stride);
+        count_launch();
     }
 
     FinArgs f;
@@ -675,14 +761,16 @@ cudaError_t launch_backward(const BwdLaunch &a, cudaStream_t s) {
     f.gate = (a.blend.flags & SS_OPT_GATE) ? 1 : 0;
     f.cam_grads = cam_grads ? 1 : 0;
     f.accumulate = (a.blend.flags & SS_OPT_ACCUMULATE) ? 1 : 0;
+    f.det = det ? 1 : 0;
     const long long fin_blocks = (M + 255) / 256;
     long long fin_grid = 148 * 4 > (fin_blocks + 7) / 8 ? 148 * 4 : (fin_blocks + 7) / 8;  // one wave (56 registers: 4 CTAs per SM) or <= 8 spheres per thread
+    if (det && fin_grid > CAM_BLOCKS_MAX - 2) fin_grid = CAM_BLOCKS_MAX - 2;  // one camera-sum slot per block
     int grid = (int)(fin_blocks < fin_grid ? fin_blocks : fin_grid);
     {
         ProfScope ps(KID_FINALIZE, s);
         k_finalize<<<grid, 256, 0, s>>>(f);
     }
-    count_launch(2);
+    count_launch();
     return cudaGetLastError();
 }
 

@@ -129,7 +129,24 @@ struct BwdLaunch {
     char *ws; Layout L;
     const int32_t *ids; const float *z, *clos, *log_denom, *upstream;
     float *d_pos, *d_rad, *d_opa, *d_feat; int32_t *pixel_count; double *cam_grad;
+    char *det_ws;  // SS_OPT_DETERMINISTIC scratch (DetLayout) or nullptr
 };
+
+// Scratch of the deterministic backward: per-sphere float bits of max |addend| (first pass), then the 64-bit
+// fixed-point accumulator rows (same AoS layout as the float rows).
+struct DetLayout {
+    size_t max_bits;  // M uint32
+    size_t raw64;     // M * raw_stride int64
+    size_t total;
+};
+inline DetLayout make_det_layout(const SsDims &dm) {
+    DetLayout D;
+    const size_t M = (size_t)(dm.num_spheres > 0 ? dm.num_spheres : 1);
+    D.max_bits = 0;
+    D.raw64 = align256(M * 4);
+    D.total = D.raw64 + align256(M * (size_t)raw_stride_for(dm.feature_dim) * 8);
+    return D;
+}
 
 cudaError_t launch_project(const FwdLaunch &a, bool records_only, cudaStream_t s);
 cudaError_t launch_binning(const FwdLaunch &a, cudaStream_t s);

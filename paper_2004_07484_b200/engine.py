@@ -98,6 +98,7 @@ class RenderEngine:
         # addresses cannot be recycled) are the ones handed to backward, unmodified (torch version counters).
         self._fwd_seq = 0
         self._last_fwd = None
+        self._det_ws: Optional[torch.Tensor] = None  # scratch of the deterministic backward
 
     # -- workspace -------------------------------------------------------------------
     def _dims(self, m, d, w, h, k, max_pairs) -> _lib.SsDims:
@@ -265,10 +266,12 @@ class RenderEngine:
     # -- backward --------------------------------------------------------------------
     def backward(self, pos, rad, opa, feat, bg, cam: CameraSpec, buf: dict, upstream, gamma, eps,
                  normalize=True, gate=True, camera_grads=True, out: Optional[dict] = None,
-                 accumulate=False, tile=16):
+                 accumulate=False, tile=16, deterministic=False):
         """Enqueue the backward pipeline.  `buf` holds ids/z/closeness (K,H,W) + log_denom (H,W)
         CUDA tensors.  Returns dict of CUDA tensors d_pos, d_rad, d_opa, d_feat, pixel_count and
-        cam_grad (16 float64: d_t[3], dL/dR[9], d_focal, d_sensor)."""
+        cam_grad (16 float64: d_t[3], dL/dR[9], d_focal, d_sensor).  deterministic=True selects the
+        bit-reproducible accumulation (SS_OPT_DETERMINISTIC: about twice the backward time), the counterpart
+        of the reference's fixed-order merge (grad.py:231-250)."""
         dev = self.device
         bg = _dev_f32(bg, dev, (-1,))
         d = bg.shape[0]
@@ -305,6 +308,16 @@ class RenderEngine:
             flags |= _lib.OPT_ACCUMULATE
         if reuse:
             flags |= _lib.OPT_REUSE_RECORDS
+        det_ws = None
+        if deterministic and m > 0:
+            flags |= _lib.OPT_DETERMINISTIC
+            nb = C.c_size_t()
+            rc = self.lib.ss_deterministic_workspace_bytes(C.byref(dims), C.byref(nb))
+            if rc != _lib.SS_OK:
+                _raise_for(rc)
+            if self._det_ws is None or self._det_ws.numel() < nb.value:
+                self._det_ws = torch.empty(nb.value, dtype=torch.uint8, device=dev)
+            det_ws = self._det_ws
         a = _lib.SsBackwardArgs()
         a.dims, a.cam = dims, cam.to_c()
         a.blend = _lib.SsBlend(float(gamma), float(eps), 0.0, int(tile), 256, flags, 0)
@@ -315,6 +328,7 @@ class RenderEngine:
         a.d_pos, a.d_rad, a.d_opa = _ptr(out["d_pos"]), _ptr(out["d_rad"]), _ptr(out["d_opa"])
         a.d_feat, a.pixel_count = _ptr(out["d_feat"]), _ptr(out["pixel_count"])
         a.cam_grad = _ptr(out.get("cam_grad"))
+        a.det_workspace, a.det_workspace_bytes = _ptr(det_ws), (det_ws.numel() if det_ws is not None else 0)
         with torch.cuda.device(dev):
             rc = self.lib.ss_backward(C.byref(a), self._stream())
         if rc != _lib.SS_OK:

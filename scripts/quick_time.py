@@ -16,6 +16,7 @@ def main():
     count = int(sys.argv[1]) if len(sys.argv) > 1 else 1_000_000
     size = int(sys.argv[2]) if len(sys.argv) > 2 else 1024
     tau = float(sys.argv[3]) if len(sys.argv) > 3 else 0.01
+    det = len(sys.argv) > 4 and sys.argv[4] == "det"  # time the SS_OPT_DETERMINISTIC backward
     steps = 10
     pos, rad, opa, feat, bg, vec = orc.benchmark_scene(count, size, size, seed=0)
     cam = camera_from_vector(vec, size, size)
@@ -38,7 +39,7 @@ def main():
             e0[i].record()
             f = eng.forward(*dev, spec, gamma=0.1, tau=tau, top_k=5, check=False)
             e1[i].record()
-            out = eng.backward(*dev, spec, f, up, gamma=0.1, eps=1e-2)
+            out = eng.backward(*dev, spec, f, up, gamma=0.1, eps=1e-2, deterministic=det)
             e2[i].record()
         torch.cuda.synchronize()
         fw = np.array([a.elapsed_time(b) for a, b in zip(e0, e1)])

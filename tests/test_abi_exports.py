@@ -40,7 +40,7 @@ def test_library_exports_every_declared_symbol(lib):
 
 
 def test_abi_version_and_status_strings(lib):
-    assert lib.ss_abi_version() == 1
+    assert lib.ss_abi_version() == 2
     assert _lib.status_string(_lib.SS_OK) == "ok"
     assert "workspace" in _lib.status_string(_lib.SS_ERR_WORKSPACE)
 

@@ -358,3 +358,55 @@ def test_backward_never_uses_stale_records(engine):
     want = fresh_engine.backward(tp_new, tr, to, tf, tb, spec, fa, up, gamma=0.1, eps=1e-2)
     assert torch.allclose(got["d_pos"], want["d_pos"], rtol=2e-5, atol=1e-9)
     assert not torch.allclose(got["d_pos"], base["d_pos"], rtol=1e-3, atol=1e-9)
+
+
+# ------------------------------------------------------------------------------------------ deterministic mode
+@pytest.mark.parametrize("count,size,d,k", [(100_000, 512, 3, 5), (20_000, 256, 16, 32), (5_000, 128, 20, 6)])
+def test_deterministic_backward_is_bit_reproducible(engine, count, size, d, k):
+    """SS_OPT_DETERMINISTIC: the counterpart of the reference's guarantee that results are bit-identical from run
+    to run (fixed-order merge, grad.py:231-250).  Two calls, a call on a FRESH engine and a call after
+    unrelated work on the same workspace must agree bit for bit in every gradient, including the camera block;
+    the values must still be the oracle's (same bars as the default path); the default path differs from run to
+    run (float32 atomics) -- if it ever becomes reproducible this test says so."""
+    import torch
+    import paper_2004_07484_b200 as pk
+    from oracle import oracle as orc
+    pos, rad, opa, feat, bg, vec = orc.benchmark_scene(count, size, size, seed=3, d=d)
+    vec = np.array(vec, dtype=np.float64)
+    vec[:6] = [0.05, -0.03, 0.1, 0.01, -0.02, 0.015]
+    spec = pk.CameraSpec.from_camera(pk.camera_from_vector(vec, size, size))
+    dev = engine.device
+    scene = tuple(torch.from_numpy(x).to(dev) for x in (pos, rad, opa, feat, bg))
+    rng = np.random.default_rng(1)
+    up = torch.from_numpy(rng.normal(size=(size, size, d)).astype(np.float32)).to(dev)
+    keys = ("d_pos", "d_rad", "d_opa", "d_feat", "pixel_count", "cam_grad")
+
+    def run(eng, deterministic):
+        f = eng.forward(*scene, spec, gamma=0.1, tau=0.0, top_k=k)
+        o = eng.backward(*scene, spec, f, up, gamma=0.1, eps=1e-2, deterministic=deterministic)
+        return {key: o[key].clone() for key in keys}
+
+    a = run(engine, True)
+    b = run(engine, True)
+    run(engine, False)  # unrelated work in between (leaves float accumulators / clean tags behind)
+    c = run(engine, True)
+    fresh = run(pk.RenderEngine(dev), True)
+    for other in (b, c, fresh):
+        for key in keys:
+            assert torch.equal(a[key], other[key]), f"{key} differs between deterministic runs"
+    ocam = orc.camera_from_vector(vec, size, size)
+    thr = orc.num_threads_available()
+    ref = orc.render_forward(pos, rad, opa, feat, bg, ocam, gamma=0.1, tau=0.0, top_k=k, threads=thr)
+    gr = orc.render_backward(pos, rad, opa, feat, bg, ocam, ref, up.cpu().numpy().astype(np.float64), threads=thr)
+    assert np.array_equal(a["pixel_count"].cpu().numpy(), gr["pixel_count"])
+    grad_close(a["d_pos"].cpu().numpy(), gr["d_position"], "deterministic d_position")
+    grad_close(a["d_rad"].cpu().numpy(), gr["d_radius"], "deterministic d_radius")
+    grad_close(a["d_opa"].cpu().numpy(), gr["d_opacity"], "deterministic d_opacity")
+    grad_close(a["d_feat"].cpu().numpy(), gr["d_feature"], "deterministic d_feature")
+    cg = a["cam_grad"].cpu().numpy()
+    grad_close(cg[0:3], gr["d_translation"], "deterministic d_translation")
+    grad_close(cg[3:12].reshape(3, 3), gr["grad_rot_matrix"], "deterministic dL/dR")
+    grad_close(cg[12:14], [gr["d_focal"], gr["d_sensor_width"]], "deterministic intrinsics")
+    if count >= 100_000:
+        x, y = run(engine, False), run(engine, False)
+        assert not all(torch.equal(x[key], y[key]) for key in keys), "the default path was reproducible here"

@@ -629,20 +629,26 @@ __global__ void __launch_bounds__(256) k_finalize(FinArgs a) {
         else if (v != 0.0) atomicAdd(&a.cam_part[lane], v);
     }
     __syncwarp();
-    if (lane != 0) return;
-    __threadfence();  // orders this block's atomics (cumulative over the warp) before the counter
-    unsigned int *counter = (unsigned int *)(a.cam_part + BST_COUNTER);
-    if (atomicAdd(counter, 1u) != gridDim.x - 1) return;
-    __threadfence();
-    if (a.cam_grads && a.det) {  // block-ordered sum of the per-block slots (lane 0 of the last block)
-        volatile double *slots = a.cam_part + CAM_VALS + 2;
-        for (int j = 0; j < 14; ++j) {
-            double acc = 0.0;
-            for (unsigned b = 0; b < gridDim.x; ++b) acc += slots[(size_t)b * CAM_VALS + j];
-            a.cam_part[j] = acc;
-        }
+    unsigned last = 0u;
+    if (lane == 0) {
+        __threadfence();  // orders this block's atomics / slot stores (cumulative over the warp) before the counter
+        unsigned int *counter = (unsigned int *)(a.cam_part + BST_COUNTER);
+        last = atomicAdd(counter, 1u) == gridDim.x - 1 ? 1u : 0u;
         __threadfence();
     }
+    last = __shfl_sync(0xffffffffu, last, 0);
+    if (!last) return;
+    if (a.cam_grads && a.det) {  // block-ordered sum of the per-block slots: lane j adds up column j
+        if (lane < 14) {
+            volatile double *slots = a.cam_part + CAM_VALS + 2;
+            double acc = 0.0;
+            for (unsigned b = 0; b < gridDim.x; ++b) acc += slots[(size_t)b * CAM_VALS + lane];
+            a.cam_part[lane] = acc;
+        }
+        __threadfence();
+        __syncwarp();
+    }
+    if (lane != 0) return;
     if (a.cam_grads) {
         const double *R = cam.R;
         volatile double *vs = a.cam_part;

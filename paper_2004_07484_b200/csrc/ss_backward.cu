@@ -522,6 +522,7 @@ __global__ void __launch_bounds__(256) k_finalize(FinArgs a) {
     // butterfly, the barrier, the float64 atomics, the fence and the (returning) completion-counter atomic at the
     // end are paid once per CTA instead of once per 256 spheres.
     const long long n_blocks = (a.M + 255) / 256;
+    const bool feat_quads = (d & 3) == 0 && (reinterpret_cast<unsigned long long>(a.d_feat) & 15ull) == 0ull;
     const float4 zero4 = make_float4(0.f, 0.f, 0.f, 0.f);
     float4 n0 = zero4, n1 = zero4;  // the first two quads of the NEXT sphere's row, loaded one iteration ahead
     {
@@ -576,11 +577,20 @@ __global__ void __launch_bounds__(256) k_finalize(FinArgs a) {
                 acc[13] = fmaf(cam_scale, r1.z, acc[13]);
             }
         }
-        // features: RS - 8 = ceil4(d) floats behind the two fixed quads
+        // features: RS - 8 = ceil4(d) floats behind the two fixed quads (whole, aligned rows move as 128-bit words)
         float *df = a.d_feat + (size_t)i * d;
         for (int q = 0; q * 4 < d; ++q) {
             float4 f4 = touched ? row[2 + q] : make_float4(0.f, 0.f, 0.f, 0.f);
             const float v[4] = {f4.x * inv_div, f4.y * inv_div, f4.z * inv_div, f4.w * inv_div};
+            if (feat_quads) {
+                float4 *dq = reinterpret_cast<float4 *>(df) + q;
+                if (a.accumulate) {
+                    if (touched) { float4 o = *dq; o.x += v[0]; o.y += v[1]; o.z += v[2]; o.w += v[3]; *dq = o; }
+                } else {
+                    *dq = make_float4(v[0], v[1], v[2], v[3]);
+                }
+                continue;
+            }
 #pragma unroll
             for (int c = 0; c < 4; ++c)
                 if (q * 4 + c < d) {

@@ -6,7 +6,7 @@ import os
 import numpy as np
 import pytest
 
-from helpers import GOLDEN_DIR, assert_close
+from helpers import GOLDEN_DIR, assert_close, make_random_scene
 
 pytestmark = pytest.mark.gpu
 
@@ -283,3 +283,45 @@ def test_fit_loop_matches_reference_trace_and_events(engine, g):
         pk.fit(sc, [], cfg)
     with pytest.raises(pk.ValidationError):
         pk.fit(sc, [pk.Observation(image=np.zeros((3, 3, 3)), camera=cams[0])], cfg)
+
+
+def test_prune_threshold_is_decided_in_float64_and_survivors_are_exact(engine):
+    """the reference-signature prune() must decide `clip(opacity) >= prune_opacity_min` on the scene's own
+    float64 values (float32(0.7) = 0.69999999 would drop a sphere the reference keeps, optim.py:169-175) and return
+    exact float64 copies of the survivors (optim.py:176-181); FitConfig accepts the reference's `workers` field."""
+    import paper_2004_07484_b200 as pk
+    rng = np.random.default_rng(2)
+    m = 64
+    sc = pk.new_scene(3, [0.1, 0.2, 0.3])
+    sc.positions = rng.uniform(-1, 1, (m, 3)) + 1e-9 / 3.0  # not float32-representable
+    sc.radii = rng.uniform(0.1, 1, m)
+    sc.opacities = np.full(m, 0.7)
+    sc.opacities[::2] = np.nextafter(0.7, 0.0)  # one ulp below the threshold: dropped
+    sc.features = rng.uniform(0, 1, (m, 3))
+    cfg = pk.FitConfig(prune_opacity_min=0.7, workers=4)
+    out, keep = pk.prune(sc, np.ones(m, dtype=np.int64), cfg)
+    assert np.array_equal(keep, np.arange(m) % 2 == 1)
+    assert out.positions.dtype == np.float64 and np.array_equal(out.positions, sc.positions[keep])
+    assert np.array_equal(out.features, sc.features[keep]) and np.array_equal(out.radii, sc.radii[keep])
+    sub = pk.subdivide(out, pk.FitConfig(subdivide_scale=0.5))
+    assert sub.positions.dtype == np.float64 and len(sub) == 12 * len(out)
+    a = out.radii / np.sqrt(2.0)
+    assert np.array_equal(sub.positions[0], out.positions[0] + a[0] * np.array([1.0, 1.0, 0.0]))
+    assert np.array_equal(sub.radii[:12], np.full(12, out.radii[0] * 0.5))
+
+
+def test_visibility_counter_saturates_instead_of_wrapping(engine):
+    """the device visibility counter is int32 where the reference sums in int64 (optim.py:307); it must
+    saturate -- a wrapped negative count would prune a fully visible sphere."""
+    import torch
+    import paper_2004_07484_b200 as pk
+    rng = np.random.default_rng(3)
+    pos, rad, opa, feat, bg = make_random_scene(rng, 50)
+    fit = pk.DeviceFit(pos, rad, opa, feat, bg, pk.FitConfig(lr_position=0.0, lr_radius=0.0, lr_opacity=0.0,
+                                                              lr_feature=1e-3, tau=0.0), engine=engine)
+    fit.visibility.fill_(2 ** 31 - 5)
+    cam = pk.CameraSpec.from_camera(pk.camera_from_vector([0, 0, 0, 0, 0, 0, 5.0, 2.0], 48, 48))
+    target = torch.zeros((48, 48, 3), device=engine.device)
+    fit.step(target, cam)
+    vis = fit.visibility.cpu().numpy()
+    assert vis.min() >= 2 ** 31 - 5 and vis.max() == 2 ** 31 - 1

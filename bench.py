@@ -442,9 +442,11 @@ def main():
             "e2e": {"value": e2e_value, "unit": "frames/s", "h2d_bytes_per_step": h2d_b, "d2h_bytes_per_step": d2h_b,
                     "steps": e2e_steps,
                     "path": "HostRenderSession.render_step (C ABI, pinned host buffers): scene resident on the device "
-                            "(uploaded by set_scene when it changes); per step upstream H2D, ss_forward, image D2H, "
-                            "ss_backward, gradient rows of the touched spheres (index + count + grads, compacted on "
-                            "the device) + camera block D2H"},
+                            "(uploaded by set_scene when it changes); per step and view upstream H2D, ss_forward, image "
+                            "D2H, ss_backward; then " +
+                            ("the gradient rows of the touched spheres (index + count + grads, compacted on the device) "
+                             "+ camera block D2H" if compact else
+                             "the allreduce of the sphere gradients and one D2H block with all M gradient rows")},
             "e2e_dense_reupload": {"value": e2e_dense, "unit": "frames/s", "h2d_bytes_per_step": dense_h2d,
                                    "d2h_bytes_per_step": dense_d2h,
                                    "path": "same call, whole scene uploaded and all M gradient rows downloaded every step "

@@ -79,11 +79,14 @@ class ViewShardedRenderer:
         the usual event; the pixel counts cannot ride in the float buffer, their sums exceed 2^24).  Backends
         without coalescing (gloo in the CPU tests) issue the two reductions back to back."""
         if self.backend == "nccl":
-            with dist._coalescing_manager(group=self.group, device=grads.flat.device, async_ops=True) as cm:
-                dist.all_reduce(grads.flat, op=dist.ReduceOp.SUM, group=self.group)
-                dist.all_reduce(grads.pixel_count, op=dist.ReduceOp.SUM, group=self.group)
-            self.collectives_issued += 1
-            return cm
+            try:
+                with dist._coalescing_manager(group=self.group, async_ops=True) as cm:
+                    dist.all_reduce(grads.flat, op=dist.ReduceOp.SUM, group=self.group)
+                    dist.all_reduce(grads.pixel_count, op=dist.ReduceOp.SUM, group=self.group)
+                self.collectives_issued += 1
+                return cm
+            except Exception:  # the (private) coalescing API moved or refused the group: two plain collectives
+                self.backend = "nccl (uncoalesced)"
         h1 = dist.all_reduce(grads.flat, op=dist.ReduceOp.SUM, group=self.group, async_op=True)
         h2 = dist.all_reduce(grads.pixel_count, op=dist.ReduceOp.SUM, group=self.group, async_op=True)
         self.collectives_issued += 2

@@ -116,12 +116,13 @@ def render_forward(scene, camera, params, *, workers: int = 1, dtype=np.float64,
     """Bounds, depth order, tile binning and tile draw on the GPU.
 
     Returns (FeatureImage, BackwardBuffer or None, RenderStats) like the reference.  `workers` is accepted
-    for signature compatibility (the device path is deterministic); `dtype` selects the dtype of the returned
+    for signature compatibility (the device path is deterministic); `tile_size` other than 16 is accepted at
+    tau = 0, where only the counters depend on it (see below); `dtype` selects the dtype of the returned
     arrays like in the reference (raster.py:462-474) -- the device arithmetic is the mixed float32 blend /
     float64 geometry path either way."""
     eng = engine or default_engine()
-    if tile_size != DEFAULT_TILE_SIZE:
-        raise ConfigurationError("the B200 path supports tile_size=16 only")
+    if int(tile_size) < 1:
+        raise ConfigurationError(f"tile_size must be >= 1, got {tile_size}")
     if not (1 <= int(chunk_size) <= 256):
         raise ConfigurationError("chunk_size must be in 1..256")
     dtype = np.dtype(dtype)
@@ -129,6 +130,14 @@ def render_forward(scene, camera, params, *, workers: int = 1, dtype=np.float64,
         raise ConfigurationError(f"dtype must be float64 or float32, got {dtype}")
     p = params if isinstance(params, BlendParams) else BlendParams(params.gamma, params.epsilon, params.tau,
                                                                    params.top_k)
+    other_tiles = int(tile_size) != DEFAULT_TILE_SIZE
+    if other_tiles and p.tau > 0.0:
+        # The device draws 16x16 tiles.  Image, buffer and gradients do not depend on the tile size at tau = 0 (only
+        # the `tiles` / `candidates_tested` counters do, and those are recomputed below); with tau > 0 the early-stop
+        # vote is taken per tile and chunk of the tile's list (raster.py:358-368), so another tile size would stop
+        # other pixels than the reference does.
+        raise ConfigurationError("tile_size != 16 is supported for tau = 0 only (the device takes the early-stop "
+                                 "vote per 16x16 tile)")
     cols = _scene_columns(scene)
     # background is validated on the host (d numbers); per-sphere fields are scanned on the device
     if not np.all(np.isfinite(np.asarray(scene.background, dtype=np.float64))):
@@ -142,7 +151,8 @@ def render_forward(scene, camera, params, *, workers: int = 1, dtype=np.float64,
         # the kernels write image | bg_weight into one device block: one D2H copy
         res = eng.forward(*dev_in, cam, gamma=p.gamma, eps=p.epsilon, tau=p.tau, top_k=p.top_k,
                           chunk=int(chunk_size), store_buffer=store_buffer, collect_stats=True, check=True,
-                          image=st.d_img[:n_img].view(h, w, d), bg_weight=st.d_img[n_img:].view(h, w))
+                          image=st.d_img[:n_img].view(h, w, d), bg_weight=st.d_img[n_img:].view(h, w),
+                          debug=other_tiles)
         stat = res["status"]
         st.h_img.copy_(st.d_img, non_blocking=True)
         torch.cuda.current_stream(eng.device).synchronize()
@@ -155,9 +165,16 @@ def render_forward(scene, camera, params, *, workers: int = 1, dtype=np.float64,
         buffer._inputs = res["inputs"]
         buffer._host_cols = cols  # strong references: ids of live objects cannot be recycled
         buffer._scene_fp = _fingerprint(cols)
-    ntx, nty = (cam.width + 15) // 16, (cam.height + 15) // 16
+    ts = int(tile_size)
+    ntx, nty = (cam.width + ts - 1) // ts, (cam.height + ts - 1) // ts
+    tested = stat["candidates_tested"]
+    if other_tiles:  # tau = 0: every tile scans its whole list, i.e. one test per (sphere, tile) pair of THAT tiling
+        rect = res["rect"].cpu().numpy().astype(np.int64)
+        on = res["on_sensor"].cpu().numpy().astype(bool)
+        pairs = (rect[:, 1] // ts - rect[:, 0] // ts + 1) * (rect[:, 3] // ts - rect[:, 2] // ts + 1)
+        tested = int(pairs[on].sum())
     stats = RenderStats(spheres_total=len(scene), spheres_on_sensor=stat["spheres_on_sensor"],
-                        candidates_tested=stat["candidates_tested"], hits_blended=stat["hits_blended"],
+                        candidates_tested=tested, hits_blended=stat["hits_blended"],
                         pixels_early_stopped=stat["pixels_early_stopped"], tiles=ntx * nty)
     return image, buffer, stats
 

@@ -68,8 +68,8 @@ def test_error_behaviour_matches_reference(engine):
         pk.render_backward(small, cam, params, buffer, np.zeros((32, 32, 3)))
     with pytest.raises(pk.ValidationError):  # upstream shape, grad.py:346-349
         pk.render_backward(scene, cam, params, buffer, np.zeros((32, 31, 3)))
-    with pytest.raises(pk.ConfigurationError):
-        pk.render_forward(scene, cam, params, tile_size=8)
+    with pytest.raises(pk.ConfigurationError):  # other tile sizes only at tau = 0 (test_other_tile_sizes_at_tau_zero)
+        pk.render_forward(scene, cam, pk.BlendParams(tau=0.01), tile_size=8)
 
 
 def test_zero_upstream_and_offscreen_sphere(engine):
@@ -333,3 +333,32 @@ def test_accumulator_reuse_protocol(engine):
         for k in ("d_pos", "d_rad", "d_opa", "d_feat"):
             grad_close(r[k].cpu().numpy(), ref[k].cpu().numpy(), k, rtol=2e-5)
         grad_close(r["cam_grad"].cpu().numpy(), ref["cam_grad"].cpu().numpy(), "cam_grad", rtol=2e-5)
+
+
+def test_other_tile_sizes_at_tau_zero(engine):
+    """The reference accepts any tile_size (raster.py:437-447).  At tau = 0 image, buffer and gradients do not
+    depend on it, only the `tiles` / `candidates_tested` counters do: checked against the REFERENCE's outputs for
+    tile sizes 8 / 24 / 32 (tests/golden/extras_tile_sizes.npz).  With tau > 0 the vote is per tile: refused."""
+    import os
+    import paper_2004_07484_b200 as pk
+    from helpers import GOLDEN_DIR
+    g = np.load(os.path.join(GOLDEN_DIR, "extras_tile_sizes.npz"))
+    scene = _scene_obj(pk, g["pos"], g["rad"], g["opa"], g["feat"], g["bg"])
+    cam = pk.camera_from_vector(g["cam_vec"], int(g["width"]), int(g["height"]))
+    p0 = pk.BlendParams(gamma=0.1, tau=0.0, top_k=5)
+    base, buf16, _ = pk.render_forward(scene, cam, p0, engine=engine)
+    up = np.random.default_rng(0).normal(size=base.data.shape)
+    g16, _ = pk.render_backward(scene, cam, p0, buf16, up, engine=engine)
+    for tile in g["tile_sizes"]:
+        image, buf, st = pk.render_forward(scene, cam, p0, tile_size=int(tile), engine=engine)
+        assert np.array_equal(buf.ids, g[f"ids_{tile}"])
+        assert_close(image.data, g[f"image_{tile}"], FWD_RTOL, FWD_ATOL, f"image, tile_size {tile}")
+        assert [st.spheres_total, st.spheres_on_sensor, st.candidates_tested, st.hits_blended,
+                st.pixels_early_stopped, st.tiles] == [int(x) for x in g[f"stats_{tile}"]]
+        gt, _ = pk.render_backward(scene, cam, p0, buf, up, tile_size=int(tile), engine=engine)
+        assert np.array_equal(gt.pixel_count, g16.pixel_count)
+        grad_close(gt.d_position, g16.d_position, f"d_position, tile_size {tile}", rtol=2e-5)
+    with pytest.raises(pk.ConfigurationError, match="tau = 0"):
+        pk.render_forward(scene, cam, pk.BlendParams(gamma=0.1, tau=0.01), tile_size=8, engine=engine)
+    with pytest.raises(pk.ConfigurationError):
+        pk.render_forward(scene, cam, p0, tile_size=0, engine=engine)

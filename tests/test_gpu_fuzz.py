@@ -112,7 +112,9 @@ def test_tile_sort_tie_paths_vs_oracle(engine, case):
     elif case == "outlier_range":     # one huge far sphere in every tile: the 23-bit parts of the rest collapse
         pos[:, 2] = rng.uniform(8.0, 8.0004, m)
         pos[0], rad[0] = (0.0, 0.0, 4000.0), 3000.0
-    elif case == "near_ties":         # keys differing in the last float64 bits only
+    elif case == "near_ties":         # 30 distinct depths on the axis: long runs of EQUAL keys (the float32 cast below
+        # removes the 2^-50 perturbation; keys that differ in their last float64 bits need a float64 camera
+        # translation and are covered by tests/test_gpu_round2.py::test_last_bit_float64_key_ties)
         base = rng.uniform(8, 30, 30)
         pos[:, 2] = base[rng.integers(0, 30, m)] * (1.0 + rng.integers(0, 4, m) * 2.0 ** -50)
         pos[:, :2] = 0.0

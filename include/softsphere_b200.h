@@ -273,11 +273,15 @@ int ss_prune_mask_f64(const double *opa, const double *feat, const double *bg, c
  * (SceneGradients.pixel_count > 0, grad.py:45-61): a host caller then compacts and downloads only those rows. */
 int ss_mask_nonzero_i32(const int32_t *values, int64_t M, uint8_t *keep, void *stream);
 
-/* One per-sphere column to compact: `row_bytes` (a multiple of 4) bytes per sphere, device pointers. */
+/* One per-sphere column to compact: `row_bytes` (a multiple of 4) bytes per sphere, device pointers.
+ * `dst_stride_bytes` = 0 packs the kept rows back to back (scene.positions[keep], optim.py:176-181); a larger
+ * multiple of 4 leaves that distance between consecutive kept rows, so that several columns can be interleaved
+ * into ONE array of records (dst pointers offset inside the first record): one copy moves them all. */
 typedef struct SsColumn {
     const void *src;
     void *dst;
     int64_t row_bytes;
+    int64_t dst_stride_bytes;
 } SsColumn;
 
 int ss_compact_workspace_bytes(int64_t M, size_t *out_bytes);

@@ -83,7 +83,7 @@ class SsFitStepArgs(C.Structure):
 
 
 class SsColumn(C.Structure):
-    _fields_ = [("src", _P), ("dst", _P), ("row_bytes", C.c_int64)]
+    _fields_ = [("src", _P), ("dst", _P), ("row_bytes", C.c_int64), ("dst_stride_bytes", C.c_int64)]
 
 
 class SsLight(C.Structure):

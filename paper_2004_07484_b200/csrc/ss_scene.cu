@@ -106,6 +106,7 @@ struct Columns {
     const unsigned *src[MAX_COLS];
     unsigned *dst[MAX_COLS];
     int words[MAX_COLS];  // 32-bit words per row
+    int stride[MAX_COLS]; // 32-bit words between consecutive destination rows (= words when packed)
     int n;
 };
 
@@ -136,11 +137,12 @@ __global__ void __launch_bounds__(CB) k_compact_rows(const unsigned char *__rest
     for (int c = 0; c < cols.n; ++c) {
         const int w = cols.words[c];
         const unsigned *src = cols.src[c] + (size_t)row0 * w;
-        unsigned *dst = cols.dst[c] + (size_t)dst0 * w;
+        const int st = cols.stride[c];
+        unsigned *dst = cols.dst[c] + (size_t)dst0 * st;
         const int n_words = total * w;
         for (int e = tid; e < n_words; e += CB) {
             const int r = e / w, j = e - r * w;
-            dst[e] = src[s_src[r] * w + j];
+            dst[r * st + j] = src[s_src[r] * w + j];
         }
     }
 }
@@ -276,6 +278,10 @@ int ss_compact_rows(const uint8_t *keep, int64_t M, const SsColumn *cols, int32_
         c.src[i] = (const unsigned *)cols[i].src;
         c.dst[i] = (unsigned *)cols[i].dst;
         c.words[i] = (int)(cols[i].row_bytes / 4);
+        if (cols[i].dst_stride_bytes != 0 &&
+            (cols[i].dst_stride_bytes < cols[i].row_bytes || cols[i].dst_stride_bytes % 4 != 0))
+            return SS_ERR_DIMS;
+        c.stride[i] = cols[i].dst_stride_bytes ? (int)(cols[i].dst_stride_bytes / 4) : c.words[i];
     }
     const int n_blocks = (int)((M + CB - 1) / CB);
     int *bc = (int *)workspace;

@@ -8,8 +8,8 @@ Transfers are packed and minimal:
     been called since the last step (a static scene stays resident on the device);
   * gradients come back either dense (ONE block: all M rows + pixel counts + the camera block) or
     `compact=True`: only the U rows of spheres that received gradient (pixel_count > 0), preceded by
-    their sphere indices -- ss_mask_nonzero_i32 + ss_compact_rows on the device, then one count read
-    and one D2H copy per column (C3: 36 MB -> 12.7 MB);
+    their sphere indices -- ss_mask_nonzero_i32 + ss_compact_rows on the device interleave them into one
+    array of records, downloaded with one copy together with the row count (C3: 36 MB -> 12.7 MB);
   * the image download runs on a second stream so that it overlaps the upstream upload (the two
     PCIe directions) and the start of the backward pass."""
 from __future__ import annotations
@@ -60,23 +60,21 @@ class PackedGradients:
 
 
 class CompactGradients:
-    """Rows of the spheres that received gradient, gathered on the device and downloaded as
-    [index | pixel_count | d_pos | d_rad | d_opa | d_feat] column blocks of `count` rows."""
-
-    COLS = (("index", 1, torch.int32), ("pixel_count", 1, torch.int32), ("d_pos", 3, torch.float32),
-            ("d_rad", 1, torch.float32), ("d_opa", 1, torch.float32), ("d_feat", None, torch.float32))
+    """Rows of the spheres that received gradient, gathered on the device into ONE array of records
+    [index i32 | pixel_count i32 | d_pos 3 | d_rad | d_opa | d_feat d] (7 + d words each) and downloaded with a
+    single copy; the host views are columns of that record array."""
 
     def __init__(self, num_spheres: int, feature_dim: int, device):
         m, d = int(num_spheres), int(feature_dim)
         self.m, self.d, self.device = m, d, device
         self.lib = _lib.load()
-        self.widths = [w if w is not None else d for _, w, _ in self.COLS]
+        self.words = 7 + d
         self.index = torch.arange(m, dtype=torch.int32, device=device)  # one-time iota (source of the index column)
         self.keep = torch.empty(max(m, 1), dtype=torch.uint8, device=device)
         self.count = torch.zeros(1, dtype=torch.int64, device=device)
         self.h_count = torch.zeros(1, dtype=torch.int64).pin_memory()
-        self.d_cols = [torch.empty(max(m, 1) * w, dtype=dt, device=device) for (_, _, dt), w in zip(self.COLS, self.widths)]
-        self.h_cols = [torch.empty(max(m, 1) * w, dtype=dt).pin_memory() for (_, _, dt), w in zip(self.COLS, self.widths)]
+        self.d_rec = torch.empty(max(m, 1) * self.words, dtype=torch.float32, device=device)
+        self.h_rec = torch.empty(max(m, 1) * self.words, dtype=torch.float32).pin_memory()
         nb = C.c_size_t()
         rc = self.lib.ss_compact_workspace_bytes(m, C.byref(nb))
         if rc != _lib.SS_OK:
@@ -88,16 +86,20 @@ class CompactGradients:
     def gather(self, grads: dict, stream) -> dict:
         """grads: dense device gradients (d_pos, d_rad, d_opa, d_feat, pixel_count).  Returns pinned host views
         of `count` rows after synchronising `stream`."""
-        m = self.m
+        m, d, words = self.m, self.d, self.words
         sp = C.c_void_p(stream.cuda_stream)
         rc = self.lib.ss_mask_nonzero_i32(_ptr(grads["pixel_count"]), m, _ptr(self.keep), sp)
         if rc != _lib.SS_OK:
             _raise_for(rc)
-        srcs = [self.index, grads["pixel_count"], grads["d_pos"], grads["d_rad"], grads["d_opa"], grads["d_feat"]]
-        arr = (_lib.SsColumn * len(srcs))()
-        for i, (s, dcol, w) in enumerate(zip(srcs, self.d_cols, self.widths)):
-            arr[i].src, arr[i].dst, arr[i].row_bytes = s.data_ptr(), dcol.data_ptr(), 4 * w
-        rc = self.lib.ss_compact_rows(_ptr(self.keep), m, arr, len(srcs), _ptr(self.ws), self.ws.numel(),
+        cols = ((self.index, 1), (grads["pixel_count"], 1), (grads["d_pos"], 3), (grads["d_rad"], 1),
+                (grads["d_opa"], 1), (grads["d_feat"], d))
+        arr = (_lib.SsColumn * len(cols))()
+        off = 0
+        for i, (src, w) in enumerate(cols):  # interleave the columns into records: dst offset inside the first record
+            arr[i].src, arr[i].dst = src.data_ptr(), self.d_rec.data_ptr() + 4 * off
+            arr[i].row_bytes, arr[i].dst_stride_bytes = 4 * w, 4 * words
+            off += w
+        rc = self.lib.ss_compact_rows(_ptr(self.keep), m, arr, len(cols), _ptr(self.ws), self.ws.numel(),
                                       _ptr(self.count), sp)
         if rc != _lib.SS_OK:
             _raise_for(rc)
@@ -105,21 +107,19 @@ class CompactGradients:
         # the previous call needed (+5 %); only when this call touched more spheres is the remainder fetched.
         est = min(m, int(self._last_count * 1.05) + 1024) if self._last_count is not None else 0
         self.h_count.copy_(self.count, non_blocking=True)
-        for dcol, hcol, w in zip(self.d_cols, self.h_cols, self.widths):
-            if est:
-                hcol[: est * w].copy_(dcol[: est * w], non_blocking=True)
+        if est:
+            self.h_rec[: est * words].copy_(self.d_rec[: est * words], non_blocking=True)
         stream.synchronize()
         n = int(self.h_count[0])
         if n > est:
-            for dcol, hcol, w in zip(self.d_cols, self.h_cols, self.widths):
-                hcol[est * w: n * w].copy_(dcol[est * w: n * w], non_blocking=True)
+            self.h_rec[est * words: n * words].copy_(self.d_rec[est * words: n * words], non_blocking=True)
             stream.synchronize()
         self._last_count = n
-        out = {"count": n}
-        for (name, _, _), hcol, w in zip(self.COLS, self.h_cols, self.widths):
-            out[name] = hcol[: n * w].view(n, w) if w > 1 else hcol[:n]
-        self.last_bytes = 8 + 4 * max(n, est) * sum(self.widths)
-        return out
+        rec = self.h_rec[: n * words].view(n, words)
+        irec = rec.view(torch.int32)
+        self.last_bytes = 8 + 4 * max(n, est) * words
+        return {"count": n, "index": irec[:, 0], "pixel_count": irec[:, 1], "d_pos": rec[:, 2:5], "d_rad": rec[:, 5],
+                "d_opa": rec[:, 6], "d_feat": rec[:, 7:], "records": rec}
 
 
 class HostRenderSession:

@@ -188,6 +188,24 @@ def _same_scene(buffer: BackwardBuffer, cols) -> bool:
     return buffer._scene_fp == _fingerprint(cols)
 
 
+def _device_record(buffer, device):
+    """The per-pixel record as the kernels want it: slot-major (K, H, W) CUDA tensors.  A buffer made by this
+    package already holds them; a buffer made by the REFERENCE's render_forward (NumPy arrays in (H, W, K) layout,
+    raster.py:97-110) is transposed and uploaded, so the two implementations' forward and backward halves can be mixed."""
+    dev = getattr(buffer, "dev", None)
+    if dev is not None:
+        return dev
+
+    def up(a, dtype):
+        a = np.asarray(a)
+        if a.ndim == 3:
+            a = np.transpose(a, (2, 0, 1))
+        return torch.from_numpy(np.ascontiguousarray(a, dtype=dtype)).to(device, non_blocking=True)
+
+    return {"ids": up(buffer.ids, np.int32), "z": up(buffer.z, np.float32), "closeness": up(buffer.closeness, np.float32),
+            "log_denom": up(buffer.log_denom, np.float32)}
+
+
 def render_backward(scene, camera, params, buffer: BackwardBuffer, upstream, *, workers: int = 1,
                     normalize: bool = True, gate: bool = True, tile_size: int = 16,
                     engine: RenderEngine = None, reuse_upload: bool = True, deterministic: bool = False):
@@ -200,7 +218,8 @@ def render_backward(scene, camera, params, buffer: BackwardBuffer, upstream, *, 
     upstream = np.asarray(upstream)
     if upstream.dtype not in (np.float64, np.float32):
         upstream = upstream.astype(np.float64)
-    k, h, w = buffer.dev["ids"].shape
+    record = _device_record(buffer, eng.device)
+    k, h, w = record["ids"].shape
     m, d = len(scene), int(scene.feature_dim)
     if upstream.shape != (h, w, d):
         raise ValidationError(f"upstream shape {upstream.shape} != {(h, w, d)}")
@@ -215,7 +234,7 @@ def render_backward(scene, camera, params, buffer: BackwardBuffer, upstream, *, 
             dev_in = _upload_scene(eng, st, cols)
         _narrow_into(st.h_up, upstream)
         st.upstream.copy_(st.h_up, non_blocking=True)
-        out = eng.backward(*dev_in, cam, buffer.dev, st.upstream, gamma=bp.gamma, eps=bp.epsilon,
+        out = eng.backward(*dev_in, cam, record, st.upstream, gamma=bp.gamma, eps=bp.epsilon,
                            normalize=normalize, gate=gate, camera_grads=True, out=dict(st.grads.dev),
                            accumulate=False, deterministic=deterministic)
         hg = st.grads.download(torch.cuda.current_stream(eng.device))

@@ -201,6 +201,12 @@ def test_reference_acceptance_checks_through_the_adapter(engine, ref):
     grad_close(got.d_feature, want.d_feature, "d_feature vs reference")
     grad_close(got_c.d_translation, want_c.d_translation, "d_translation vs reference")
     grad_close(got_c.d_rotation, want_c.d_rotation, "d_rotation vs reference")
-    # the adapter's buffer is accepted by the reference's own backward (same layout and meaning)
+    # the adapter's buffer is accepted by the reference's own backward (same layout and meaning) ...
     cross, _ = ref.render_backward(scene, cam, params, buffer, up)
     grad_close(cross.d_feature, want.d_feature, "reference backward on the adapter's buffer")
+    # ... and the reference's own buffer (NumPy, (H, W, K)) by the adapter's backward
+    mixed, mixed_c = r.backward(scene, cam, params, ref_buffer, up)
+    assert np.array_equal(mixed.pixel_count, want.pixel_count)
+    grad_close(mixed.d_position, want.d_position, "adapter backward on the reference's buffer")
+    grad_close(mixed.d_feature, want.d_feature, "adapter backward on the reference's buffer (features)")
+    grad_close(mixed_c.d_translation, want_c.d_translation, "adapter backward on the reference's buffer (camera)")

@@ -442,8 +442,9 @@ def main():
             "e2e": {"value": e2e_value, "unit": "frames/s", "h2d_bytes_per_step": h2d_b, "d2h_bytes_per_step": d2h_b,
                     "steps": e2e_steps,
                     "path": "HostRenderSession.render_step (C ABI, pinned host buffers): scene resident on the device "
-                            "(uploaded by set_scene when it changes); per step and view upstream H2D, ss_forward, image "
-                            "D2H, ss_backward; then " +
+                            "(uploaded by set_scene when it changes), argument blocks prepared once; per step and view upstream "
+                            "H2D, ss_forward (last view: ss_forward_banded, 4 bands of tile rows, each band's image rows "
+                            "downloaded as soon as its event completes), image D2H, ss_backward; then " +
                             ("the gradient rows of the touched spheres (index + count + grads, compacted on the device) "
                              "+ camera block D2H" if compact else
                              "the allreduce of the sphere gradients and one D2H block with all M gradient rows")},

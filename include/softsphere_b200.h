@@ -201,6 +201,17 @@ int ss_workspace_init(const SsDims *dims, void *workspace, size_t workspace_byte
 int ss_forward(const SsForwardArgs *args, void *stream);
 int ss_backward(const SsBackwardArgs *args, void *stream);
 
+/* ss_forward with the image drawn in `n_bands` (1..SS_MAX_BANDS) bands of whole tile rows, top to bottom, one
+ * raster launch per band.  band_events: HOST array of n_bands cudaEvent_t (as void*), created by the caller;
+ * event b is recorded on `stream` right after band b and completes when rows [row_begin, row_end) of
+ * ss_band_rows(height, n_bands, b) are final in image / bg_weight / ids / z / closeness / log_denom.  A host
+ * caller lets a copy stream wait on event b and downloads those image rows while the later bands are still being
+ * drawn (the reference returns the whole image at once, raster.py:504-512; results are identical to ss_forward:
+ * tiles are independent).  The status counters are complete after the last band. */
+#define SS_MAX_BANDS 16
+int ss_forward_banded(const SsForwardArgs *args, int n_bands, void *const *band_events, void *stream);
+int ss_band_rows(int height, int n_bands, int band, int *row_begin, int *row_end);
+
 /* Scratch size of the SS_OPT_DETERMINISTIC backward for these dimensions (per-sphere grid exponents +
  * 64-bit fixed-point accumulator rows). */
 int ss_deterministic_workspace_bytes(const SsDims *dims, size_t *out_bytes);

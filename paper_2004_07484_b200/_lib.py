@@ -98,7 +98,7 @@ class SsStatus(C.Structure):
 
 
 EXPORTS = ("ss_abi_version", "ss_status_string", "ss_last_cuda_error", "ss_workspace_bytes", "ss_workspace_init",
-           "ss_forward", "ss_backward", "ss_deterministic_workspace_bytes", "ss_read_status", "ss_photometric_loss", "ss_fit_step", "ss_adam_flat", "ss_debug_tile_lists", "ss_launch_count",
+           "ss_forward", "ss_forward_banded", "ss_band_rows", "ss_backward", "ss_deterministic_workspace_bytes", "ss_read_status", "ss_photometric_loss", "ss_fit_step", "ss_adam_flat", "ss_debug_tile_lists", "ss_launch_count",
            "ss_prune_mask", "ss_prune_mask_f64", "ss_subdivide_f64", "ss_mask_nonzero_i32", "ss_compact_workspace_bytes", "ss_compact_rows", "ss_subdivide",
            "ss_psc1_unpack", "ss_psc1_pack", "ss_convert_f64_f32", "ss_convert_f32_f64",
            "ss_shade_identity", "ss_shade_identity_backward", "ss_shade_diffuse", "ss_shade_diffuse_backward",
@@ -131,6 +131,10 @@ def load():
     lib.ss_workspace_init.argtypes = [C.POINTER(SsDims), C.c_void_p, C.c_size_t, C.c_void_p]
     lib.ss_forward.restype = C.c_int
     lib.ss_forward.argtypes = [C.POINTER(SsForwardArgs), C.c_void_p]
+    lib.ss_forward_banded.restype = C.c_int
+    lib.ss_forward_banded.argtypes = [C.POINTER(SsForwardArgs), C.c_int, C.POINTER(C.c_void_p), C.c_void_p]
+    lib.ss_band_rows.restype = C.c_int
+    lib.ss_band_rows.argtypes = [C.c_int, C.c_int, C.c_int, C.POINTER(C.c_int), C.POINTER(C.c_int)]
     lib.ss_backward.restype = C.c_int
     lib.ss_backward.argtypes = [C.POINTER(SsBackwardArgs), C.c_void_p]
     lib.ss_deterministic_workspace_bytes.restype = C.c_int

@@ -35,14 +35,15 @@ def _stale() -> bool:
     return any(os.path.getmtime(d) > t for d in deps)
 
 
-def build(force: bool = False, verbose: bool = False, extra_flags=()) -> str:
-    if not force and not _stale():
+def build(force: bool = False, verbose: bool = False, extra_flags=(), out: str = None) -> str:
+    """out: build a variant (kernel experiments, selected at run time with SS_B200_LIB) next to its own objects."""
+    if out is None and not force and not _stale():
         return LIB
     nvcc = _nvcc()
     objs = []
 
     def compile_one(src):
-        obj = os.path.join(CSRC, src.replace(".cu", ".o"))
+        obj = (out + "." if out else os.path.join(CSRC, "")) + src.replace(".cu", ".o")
         cmd = [nvcc, *NVCC_FLAGS, *extra_flags, "-c", os.path.join(CSRC, src), "-o", obj]
         r = subprocess.run(cmd, capture_output=True, text=True)
         if r.returncode != 0:
@@ -53,14 +54,16 @@ def build(force: bool = False, verbose: bool = False, extra_flags=()) -> str:
 
     with ThreadPoolExecutor(max_workers=len(SOURCES)) as pool:
         objs = list(pool.map(compile_one, SOURCES))
-    cmd = [nvcc, "-shared", "-o", LIB, *objs, "-gencode", "arch=compute_100a,code=sm_100a"]
+    cmd = [nvcc, "-shared", "-o", out or LIB, *objs, "-gencode", "arch=compute_100a,code=sm_100a"]
     r = subprocess.run(cmd, capture_output=True, text=True)
     if r.returncode != 0:
         raise RuntimeError(f"link failed:\n{r.stdout}\n{r.stderr}")
-    return LIB
+    return out or LIB
 
 
 if __name__ == "__main__":
     v = "-v" in sys.argv
     extra = [a for a in sys.argv[1:] if a.startswith("-D")]
-    print(build(force=True, verbose=v, extra_flags=tuple(extra) + (("-Xptxas", "-v") if v else ())))
+    outs = [a[len("--out="):] for a in sys.argv[1:] if a.startswith("--out=")]
+    print(build(force=True, verbose=v, extra_flags=tuple(extra) + (("-Xptxas", "-v") if v else ()),
+                out=os.path.abspath(outs[0]) if outs else None))

@@ -151,7 +151,30 @@ int ss_workspace_init(const SsDims *dims, void *workspace, size_t workspace_byte
     return SS_OK;
 }
 
-int ss_forward(const SsForwardArgs *a, void *stream) {
+static int forward_impl(const SsForwardArgs *a, int n_bands, void *const *band_events, void *stream);
+
+int ss_forward(const SsForwardArgs *a, void *stream) { return forward_impl(a, 1, nullptr, stream); }
+
+int ss_forward_banded(const SsForwardArgs *a, int n_bands, void *const *band_events, void *stream) {
+    if (n_bands < 1 || n_bands > SS_MAX_BANDS) return SS_ERR_PARAMS;
+    if (!band_events) return SS_ERR_NULL;
+    for (int b = 0; b < n_bands; ++b)
+        if (!band_events[b]) return SS_ERR_NULL;
+    return forward_impl(a, n_bands, band_events, stream);
+}
+
+int ss_band_rows(int height, int n_bands, int band, int *row_begin, int *row_end) {
+    if (!row_begin || !row_end) return SS_ERR_NULL;
+    if (height < 1 || n_bands < 1 || n_bands > SS_MAX_BANDS || band < 0 || band >= n_bands) return SS_ERR_PARAMS;
+    const int nty = (height + SS_TILE - 1) / SS_TILE;
+    const int r0 = (int)((long long)nty * band / n_bands) * SS_TILE;
+    const int r1 = (int)((long long)nty * (band + 1) / n_bands) * SS_TILE;
+    *row_begin = r0 < height ? r0 : height;
+    *row_end = r1 < height ? r1 : height;
+    return SS_OK;
+}
+
+static int forward_impl(const SsForwardArgs *a, int n_bands, void *const *band_events, void *stream) {
     if (!a) return SS_ERR_NULL;
     int rc = check_dims(a->dims);
     if (rc == SS_OK) rc = check_camera(a->cam, a->dims);
@@ -174,8 +197,20 @@ int ss_forward(const SsForwardArgs *a, void *stream) {
     if (e != cudaSuccess) return cuda_fail(e);
     e = launch_binning(f, s);
     if (e != cudaSuccess) return cuda_fail(e);
-    e = launch_raster(f, s);
-    if (e != cudaSuccess) return cuda_fail(e);
+    if (n_bands <= 1 && !band_events) {
+        e = launch_raster(f, s);
+        if (e != cudaSuccess) return cuda_fail(e);
+        return SS_OK;
+    }
+    // bands of whole tile rows, one raster launch each; the event after band b completes when rows
+    // [ss_band_rows(b)) of every forward output are final (a copy stream can start downloading them)
+    for (int b = 0; b < n_bands; ++b) {
+        const int ty0 = (int)((long long)f.L.nty * b / n_bands), ty1 = (int)((long long)f.L.nty * (b + 1) / n_bands);
+        e = launch_raster(f, s, ty0 * f.L.ntx, (ty1 - ty0) * f.L.ntx);
+        if (e != cudaSuccess) return cuda_fail(e);
+        e = cudaEventRecord((cudaEvent_t)band_events[b], s);
+        if (e != cudaSuccess) return cuda_fail(e);
+    }
     return SS_OK;
 }
 

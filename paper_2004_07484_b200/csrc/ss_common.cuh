@@ -150,7 +150,8 @@ inline DetLayout make_det_layout(const SsDims &dm) {
 
 cudaError_t launch_project(const FwdLaunch &a, bool records_only, cudaStream_t s);
 cudaError_t launch_binning(const FwdLaunch &a, cudaStream_t s);
-cudaError_t launch_raster(const FwdLaunch &a, cudaStream_t s);
+// draws tiles [tile0, tile0 + n_tiles) (n_tiles < 0: to the last tile)
+cudaError_t launch_raster(const FwdLaunch &a, cudaStream_t s, int tile0 = 0, int n_tiles = -1);
 cudaError_t launch_backward(const BwdLaunch &a, cudaStream_t s);
 
 void count_launch(int n = 1);

@@ -35,6 +35,7 @@ struct RasterArgs {
     const float *feat;
     const float *bg;
     int d, K, chunk;
+    int tile0;  // first tile of this launch (ss_forward_banded draws the image in bands of tile rows)
     double gamma, eps_over_g, log_tau;
     // float32 depth used for the blend exponent and as a pre-filter of the top-K (the float64 depth is only
     // formed for hits that can enter the record): far, far - near, 1 / (far - near), error pad of the pre-filter
@@ -213,7 +214,7 @@ __global__ void __launch_bounds__(TILE_PX, (KT <= 8 && DP <= 4) ? SS_RASTER_MINB
     __shared__ unsigned long long s_stat[3];
 
     const Cam &cam = a.cam;
-    const int tile = blockIdx.x;
+    const int tile = blockIdx.x + a.tile0;
     const int tid = threadIdx.x;
     const int lane = tid & 31, warp = tid >> 5;
     // each warp owns an 8x4 pixel block of the 16x16 tile (2 x 4 blocks): a sphere footprint
@@ -592,7 +593,7 @@ void launch_k(const RasterArgs &r, int n_tiles, int mode, cudaStream_t s) {
 
 }  // namespace
 
-cudaError_t launch_raster(const FwdLaunch &a, cudaStream_t s) {
+cudaError_t launch_raster(const FwdLaunch &a, cudaStream_t s, int tile0, int n_tiles) {
     const Layout &L = a.L;
     RasterArgs r;
     r.cam = a.cam;
@@ -616,12 +617,15 @@ cudaError_t launch_raster(const FwdLaunch &a, cudaStream_t s) {
     r.image = a.image; r.bg_weight = a.bg_weight;
     r.ids = a.ids; r.z = a.z; r.clos = a.clos; r.log_denom = a.log_denom;
     r.status = (long long *)(a.ws + L.status);
+    if (n_tiles < 0) n_tiles = L.n_tiles - tile0;
+    r.tile0 = tile0;
+    if (n_tiles <= 0) return cudaSuccess;
     const int d = r.d, mode = a.cam.mode;
     ProfScope ps(KID_RASTER, s);
-    if (d == 3) launch_k<3>(r, L.n_tiles, mode, s);
-    else if (d <= 4) launch_k<4>(r, L.n_tiles, mode, s);
-    else if (d <= 16) launch_k<16>(r, L.n_tiles, mode, s);
-    else launch_k<32>(r, L.n_tiles, mode, s);
+    if (d == 3) launch_k<3>(r, n_tiles, mode, s);
+    else if (d <= 4) launch_k<4>(r, n_tiles, mode, s);
+    else if (d <= 16) launch_k<16>(r, n_tiles, mode, s);
+    else launch_k<32>(r, n_tiles, mode, s);
     count_launch();
     return cudaGetLastError();
 }

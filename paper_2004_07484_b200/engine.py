@@ -168,10 +168,14 @@ class RenderEngine:
     # -- forward ---------------------------------------------------------------------
     def forward(self, pos, rad, opa, feat, bg, cam: CameraSpec, gamma=0.1, eps=1e-2, tau=0.01, top_k=5,
                 chunk=256, tile=16, store_buffer=True, collect_stats=False, validate=True,
-                check=True, debug=False, image=None, bg_weight=None):
+                check=True, debug=False, image=None, bg_weight=None, band_events=None):
         """Enqueue the forward pipeline.  Inputs: float32 CUDA tensors (or array-likes, which are
         copied to the device).  Returns a dict of CUDA tensors; with check=True the status block
-        is read back (one stream sync), validation / overflow are handled and `status` is set."""
+        is read back (one stream sync), validation / overflow are handled and `status` is set.
+
+        band_events: a list of torch.cuda.Event -- the image is then drawn in that many bands of tile rows
+        (ss_forward_banded) and event b is recorded when the rows `band_rows(height, n, b)` are final, so that a
+        copy stream can download the upper bands while the lower ones are still being drawn."""
         dev = self.device
         bg = _dev_f32(bg, dev, (-1,))
         d = bg.shape[0]
@@ -226,7 +230,15 @@ class RenderEngine:
             a.rect, a.on_sensor = _ptr(dbg.get("rect")), _ptr(dbg.get("on_sensor"))
             a.earliest, a.proj_radius_px = _ptr(dbg.get("earliest")), _ptr(dbg.get("proj_radius_px"))
             with torch.cuda.device(dev):  # kernels launch on the current device: make it the engine's
-                rc = self.lib.ss_forward(C.byref(a), self._stream())
+                if band_events:
+                    stream = torch.cuda.current_stream(dev)
+                    for e in band_events:  # a torch event only gets its CUDA handle on first record
+                        if not e.cuda_event:
+                            e.record(stream)
+                    evs = (C.c_void_p * len(band_events))(*[C.c_void_p(e.cuda_event) for e in band_events])
+                    rc = self.lib.ss_forward_banded(C.byref(a), len(band_events), evs, self._stream())
+                else:
+                    rc = self.lib.ss_forward(C.byref(a), self._stream())
             if rc != _lib.SS_OK:
                 _raise_for(rc)
             if not check:
@@ -250,6 +262,14 @@ class RenderEngine:
                "inputs": (pos, rad, opa, feat, bg), "fwd_token": token}
         out.update(dbg)
         return out
+
+    def band_rows(self, height: int, n_bands: int, band: int):
+        """(row_begin, row_end) of band `band` when an image of `height` rows is drawn in `n_bands` bands."""
+        r0, r1 = C.c_int(), C.c_int()
+        rc = self.lib.ss_band_rows(int(height), int(n_bands), int(band), C.byref(r0), C.byref(r1))
+        if rc != _lib.SS_OK:
+            _raise_for(rc)
+        return r0.value, r1.value
 
     def tile_lists(self, m, d, w, h, k):
         """(tile_starts, sphere ids grouped by tile in scan order) of the last forward (parity)."""

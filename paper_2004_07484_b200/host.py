@@ -11,7 +11,9 @@ Transfers are packed and minimal:
     their sphere indices -- ss_mask_nonzero_i32 + ss_compact_rows on the device interleave them into one
     array of records, downloaded with one copy together with the row count (C3: 36 MB -> 12.7 MB);
   * the image download runs on a second stream so that it overlaps the upstream upload (the two
-    PCIe directions) and the start of the backward pass."""
+    PCIe directions); the forward pass draws the image in `bands` bands of tile rows (ss_forward_banded) and
+    every band is downloaded as soon as it is final -- the upper bands under the raster kernel of the lower
+    ones, the last one under the backward pass."""
 from __future__ import annotations
 
 import ctypes as C
@@ -124,7 +126,7 @@ class CompactGradients:
 
 class HostRenderSession:
     def __init__(self, num_spheres: int, feature_dim: int, width: int, height: int, top_k: int = 5,
-                 engine: RenderEngine = None, device="cuda"):
+                 engine: RenderEngine = None, device="cuda", bands: int = 4):
         self.engine = engine or RenderEngine(device)
         dev = self.engine.device
         m, d, w, h = int(num_spheres), int(feature_dim), int(width), int(height)
@@ -150,14 +152,87 @@ class HostRenderSession:
         self.upstream = torch.empty((h, w, d), dtype=f32, device=dev)
         self.h_image = torch.empty((h, w, d), dtype=f32).pin_memory()
 
+        # forward outputs and the argument blocks of the two C calls are allocated / filled once: the per-step
+        # Python work before the first kernel launch is GPU idle time on this path (it was 0.1 ms of a 1 ms step)
+        k = self.k
+        # two image buffers, alternating by view: the download of view i must not hold back the forward of view i + 1
+        self._images = [torch.empty((h, w, d), dtype=f32, device=dev) for _ in range(2)]
+        self._image_copied = [torch.cuda.Event(), torch.cuda.Event()]
+        self.bg_weight = torch.empty((h, w), dtype=f32, device=dev)
+        self.ids = torch.empty((k, h, w), dtype=torch.int32, device=dev)
+        self.z = torch.empty((k, h, w), dtype=f32, device=dev)
+        self.closeness = torch.empty((k, h, w), dtype=f32, device=dev)
+        self.log_denom = torch.empty((h, w), dtype=f32, device=dev)
+        self._prep_key = None
+        self._fa = self._ba = None
+
         self.packed = PackedGradients(m, d, dev)
         self.out, self.h_grads = self.packed.dev, self.packed.host
         self.d_out, self.h_out = self.packed.d_out, self.packed.h_out
         self._compact = None
         self.copy_stream = torch.cuda.Stream(device=dev)
+        self.bands = max(1, int(bands))
+        self._band_events = [torch.cuda.Event() for _ in range(self.bands)]
+        self._band_rows = [self.engine.band_rows(h, self.bands, b) for b in range(self.bands)]
         self._scene_dirty = True
         self.last_h2d_bytes = 0
         self.last_d2h_bytes = 0
+
+    def _prepared(self):
+        """Argument blocks of ss_forward / ss_backward with every pointer filled in; rebuilt only when the engine's
+        workspace moved or was re-laid out (the engine may be shared with other callers)."""
+        eng = self.engine
+        dims = eng._ensure_workspace(self.m, self.d, self.w, self.h, self.k)
+        key = (eng._ws.data_ptr(), eng._ws.numel(), int(dims.max_pairs))
+        if key != self._prep_key:
+            fa, ba = _lib.SsForwardArgs(), _lib.SsBackwardArgs()
+            for a in (fa, ba):
+                a.dims = dims
+                a.pos, a.rad, a.opa, a.feat, a.bg = (_ptr(self.pos), _ptr(self.rad), _ptr(self.opa), _ptr(self.feat),
+                                                     _ptr(self.bg))
+                a.workspace, a.workspace_bytes = _ptr(eng._ws), eng._ws.numel()
+                a.ids, a.z, a.closeness, a.log_denom = (_ptr(self.ids), _ptr(self.z), _ptr(self.closeness),
+                                                        _ptr(self.log_denom))
+            fa.bg_weight = _ptr(self.bg_weight)
+            ba.upstream = _ptr(self.upstream)
+            o = self.out
+            ba.d_pos, ba.d_rad, ba.d_opa, ba.d_feat = _ptr(o["d_pos"]), _ptr(o["d_rad"]), _ptr(o["d_opa"]), _ptr(o["d_feat"])
+            ba.pixel_count, ba.cam_grad = _ptr(o["pixel_count"]), _ptr(o["cam_grad"])
+            self._fa, self._ba, self._prep_key = fa, ba, key
+            self._events_c = None
+        return self._fa, self._ba
+
+    def _forward_fast(self, cam, gamma, eps, tau, events, stream, image):
+        """ss_forward[_banded] on the session's own buffers without the engine's per-call checks and allocations
+        (no status read: the caller polls engine.read_status(), like engine.forward(check=False))."""
+        fa, _ = self._prepared()
+        fa.cam, fa.image = cam.to_c(), _ptr(image)
+        fa.blend = _lib.SsBlend(float(gamma), float(eps), float(tau), 16, 256, _lib.OPT_STORE_BUFFER, 0)
+        lib, sp = self.engine.lib, C.c_void_p(stream.cuda_stream)
+        if events:
+            if self._events_c is None or len(self._events_c) != len(events):
+                for e in events:  # a torch event only gets its CUDA handle on first record
+                    if not e.cuda_event:
+                        e.record(stream)
+                self._events_c = (C.c_void_p * len(events))(*[C.c_void_p(e.cuda_event) for e in events])
+            rc = lib.ss_forward_banded(C.byref(fa), len(events), self._events_c, sp)
+        else:
+            rc = lib.ss_forward(C.byref(fa), sp)
+        if rc != _lib.SS_OK:
+            _raise_for(rc)
+        self.engine._last_fwd = None  # (the engine's own record-reuse bookkeeping does not cover this call)
+
+    def _backward_fast(self, cam, gamma, eps, normalize, gate, accumulate, stream):
+        _, ba = self._prepared()
+        ba.cam = cam.to_c()
+        # the draw records in the workspace are those of the forward call just made on the same, untouched inputs
+        flags = _lib.OPT_CAMERA_GRADS | _lib.OPT_REUSE_RECORDS
+        flags |= (_lib.OPT_NORMALIZE if normalize else 0) | (_lib.OPT_GATE if gate else 0)
+        flags |= _lib.OPT_ACCUMULATE if accumulate else 0
+        ba.blend = _lib.SsBlend(float(gamma), float(eps), 0.0, 16, 256, flags, 0)
+        rc = self.engine.lib.ss_backward(C.byref(ba), C.c_void_p(stream.cuda_stream))
+        if rc != _lib.SS_OK:
+            _raise_for(rc)
 
     def set_scene(self, pos, rad, opa, feat, bg):
         """Stage a (new) scene: uploaded by the next render_step, resident afterwards."""
@@ -189,23 +264,49 @@ class HostRenderSession:
                 self.copy_stream.wait_stream(main)  # (orders it after the previous view's backward)
                 with torch.cuda.stream(self.copy_stream):
                     self.upstream.copy_(self.h_upstream, non_blocking=True)
-            f = self.engine.forward(self.pos, self.rad, self.opa, self.feat, self.bg, cam, gamma=gamma, eps=eps,
-                                    tau=tau, top_k=self.k, check=check)
-            image = f["image"]
+            # the image is drawn in bands of tile rows; the copy stream downloads band b as soon as its event has
+            # completed, i.e. while the raster kernel of band b + 1 is running (and the last band under the backward)
+            # Only the LAST view of a step is banded: an earlier view's download hides under the next view's
+            # forward pass anyway, and a band boundary costs a few microseconds of raster time.
+            nb = self.bands if (not check and i == len(cams) - 1) else 1  # (check=True may re-render after a regrowth)
+            events = self._band_events[:nb] if nb > 1 else None
+            if i > 1:  # this image buffer was last used two views ago: its download must have read it
+                main.wait_event(self._image_copied[i & 1])
+            if check:
+                f = self.engine.forward(self.pos, self.rad, self.opa, self.feat, self.bg, cam, gamma=gamma, eps=eps,
+                                        tau=tau, top_k=self.k, check=True, band_events=events)
+                image = f["image"]
+            else:
+                image = self._images[i & 1]
+                with torch.cuda.device(dev):
+                    self._forward_fast(cam, gamma, eps, tau, events, main, image)
+                f = None
             if upstream_fn is None:
                 main.wait_stream(self.copy_stream)  # backward needs the uploaded upstream
-            self.copy_stream.wait_stream(main)
-            with torch.cuda.stream(self.copy_stream):  # image download overlaps the backward pass
-                self.h_image.copy_(image, non_blocking=True)
+            with torch.cuda.stream(self.copy_stream):
+                if events:
+                    for b, ev in enumerate(events):
+                        r0, r1 = self._band_rows[b]
+                        self.copy_stream.wait_event(ev)
+                        if r1 > r0:
+                            self.h_image[r0:r1].copy_(image[r0:r1], non_blocking=True)
+                else:
+                    self.copy_stream.wait_stream(main)
+                    self.h_image.copy_(image, non_blocking=True)
                 image.record_stream(self.copy_stream)
+                self._image_copied[i & 1].record(self.copy_stream)
             if upstream_fn is not None:
                 self.copy_stream.synchronize()
                 self.h_upstream.copy_(upstream_fn(i, self.h_image))
                 self.upstream.copy_(self.h_upstream, non_blocking=True)
             h2d += 4 * self.h_upstream.numel()
-            self.engine.backward(self.pos, self.rad, self.opa, self.feat, self.bg, cam, f, self.upstream,
-                                 gamma=gamma, eps=eps, normalize=normalize, gate=gate, camera_grads=True,
-                                 out=self.out, accumulate=(i > 0))
+            if f is not None:
+                self.engine.backward(self.pos, self.rad, self.opa, self.feat, self.bg, cam, f, self.upstream,
+                                     gamma=gamma, eps=eps, normalize=normalize, gate=gate, camera_grads=True,
+                                     out=self.out, accumulate=(i > 0))
+            else:
+                with torch.cuda.device(dev):
+                    self._backward_fast(cam, gamma, eps, normalize, gate, i > 0, main)
         if reduce_fn is not None:
             reduce_fn(self.out)
         d2h = len(cams) * 4 * self.h_image.numel()

@@ -29,13 +29,18 @@ def main():
     out = eng.backward(*dev, spec, f, up, gamma=0.1, eps=1e-2)
     torch.cuda.synchronize()
     flush = torch.empty(256 << 20, dtype=torch.uint8, device="cuda")
+    # QT_FLUSH=drain: read a second buffer after the write so that the dirty lines are written back before the frame
+    drain = torch.zeros(32 << 20, dtype=torch.int64, device="cuda") if os.environ.get("QT_FLUSH") == "drain" else None
     for collect in (False, True):
         _lib.profile_enable(collect)
         e0 = [torch.cuda.Event(enable_timing=True) for _ in range(steps)]
         e1 = [torch.cuda.Event(enable_timing=True) for _ in range(steps)]
         e2 = [torch.cuda.Event(enable_timing=True) for _ in range(steps)]
         for i in range(steps):
-            flush.zero_()
+            if os.environ.get("QT_FLUSH") != "none":
+                flush.zero_()
+            if drain is not None:
+                drain.sum()
             e0[i].record()
             f = eng.forward(*dev, spec, gamma=0.1, tau=tau, top_k=5, check=False)
             e1[i].record()

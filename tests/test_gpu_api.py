@@ -362,3 +362,42 @@ def test_other_tile_sizes_at_tau_zero(engine):
         pk.render_forward(scene, cam, pk.BlendParams(gamma=0.1, tau=0.01), tile_size=8, engine=engine)
     with pytest.raises(pk.ConfigurationError):
         pk.render_forward(scene, cam, p0, tile_size=0, engine=engine)
+
+
+@pytest.mark.parametrize("n_bands", [1, 2, 3, 7, 16])
+def test_banded_forward_is_identical_and_bands_complete_in_order(engine, n_bands):
+    """ss_forward_banded draws the image in bands of tile rows (one raster launch each) and records an event per
+    band so that a host caller can download the upper rows early.  Tiles are independent: every output and every
+    counter must equal the single-launch forward bit for bit, for band counts that do not divide the tile rows
+    (H = 100: 7 tile rows) and for more bands than tile rows (empty bands)."""
+    import torch
+    import paper_2004_07484_b200 as pk
+    from paper_2004_07484_b200.synthetic import benchmark_scene
+    w, h = 136, 100
+    pos, rad, opa, feat, bg, vec = benchmark_scene(20000, w, h, seed=3)
+    spec = pk.CameraSpec.from_camera(pk.camera_from_vector(vec, w, h))
+    ref = engine.forward(pos, rad, opa, feat, bg, spec, gamma=0.1, tau=0.01, collect_stats=True)
+    events = [torch.cuda.Event() for _ in range(n_bands)]
+    out = engine.forward(pos, rad, opa, feat, bg, spec, gamma=0.1, tau=0.01, collect_stats=True, band_events=events)
+    for k in ("image", "bg_weight", "ids", "z", "closeness", "log_denom"):
+        assert torch.equal(out[k], ref[k]), k
+    for k in ("num_pairs", "candidates_tested", "hits_blended", "pixels_early_stopped", "spheres_on_sensor"):
+        assert out["status"][k] == ref["status"][k], k
+    rows = [engine.band_rows(h, n_bands, b) for b in range(n_bands)]
+    assert rows[0][0] == 0 and rows[-1][1] == h
+    for (a0, a1), (b0, b1) in zip(rows, rows[1:]):
+        assert a1 == b0 and a0 <= a1  # contiguous, top to bottom
+    assert all(r0 % 16 == 0 for r0, _ in rows)
+    torch.cuda.synchronize()
+    assert all(e.query() for e in events)
+    # rows of band b are final once event b has completed: download band by band on a second stream
+    side = torch.cuda.Stream()
+    host = torch.empty((h, w, 3), dtype=torch.float32).pin_memory()
+    out2 = engine.forward(pos, rad, opa, feat, bg, spec, gamma=0.1, tau=0.01, check=False, band_events=events)
+    with torch.cuda.stream(side):
+        for (r0, r1), e in zip(rows, events):
+            side.wait_event(e)
+            if r1 > r0:
+                host[r0:r1].copy_(out2["image"][r0:r1], non_blocking=True)
+    side.synchronize()
+    assert np.array_equal(host.numpy(), ref["image"].cpu().numpy())

@@ -493,9 +493,8 @@ struct SegSrc {
 // pk[0 .. n) is sorted by the key part of the packed words (index part: IDX_BITS low bits).  Words in a run of
 // equal key parts are ranked exactly by (key, id); returns false, writing nothing, when more than a quarter of
 // the words tie (the caller then runs the 64-bit network).  Block-wide call.
-template <int IDX_BITS>
-__device__ bool rank_ties_and_write(const unsigned *pk, int n, const unsigned long long *keys, const int *ids,
-                                    int *out) {
+template <int IDX_BITS, typename KeyFn>
+__device__ bool rank_ties_and_write(const unsigned *pk, int n, KeyFn keys, const int *ids, int *out) {
     __shared__ int s_ties[8];
     constexpr unsigned IDX_MASK = (1u << IDX_BITS) - 1u;
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
@@ -520,12 +519,12 @@ __device__ bool rank_ties_and_write(const unsigned *pk, int n, const unsigned lo
         if (total > 0 && ((p > 0 && (pk[p - 1] >> IDX_BITS) == q) || (p + 1 < n && (pk[p + 1] >> IDX_BITS) == q))) {
             int a = p;
             while (a > 0 && (pk[a - 1] >> IDX_BITS) == q) --a;
-            const unsigned long long km = keys[me];
+            const unsigned long long km = keys(me);
             const int im = ids[me];
             int rank = 0;
             for (int j = a; j < n && (pk[j] >> IDX_BITS) == q; ++j) {
                 const int o = (int)(pk[j] & IDX_MASK);
-                rank += pair_less(keys[o], ids[o], km, im) ? 1 : 0;
+                rank += pair_less(keys(o), ids[o], km, im) ? 1 : 0;
             }
             dst = a + rank;
         }
@@ -598,7 +597,7 @@ __device__ bool sort_packed512(int s0, int n, int np2, const SegSrc &src, int *p
         if (warp == 0) { pk[i0] = e0; pk[i1] = e1; }
         __syncthreads();
     }
-    return rank_ties_and_write<9>(pk, n, keys, ids, pair_id + s0);
+    return rank_ties_and_write<9>(pk, n, [keys](int i) { return keys[i]; }, ids, pair_id + s0);
 }
 
 // The same for segments of up to 4096 pairs (12 position bits, 20 key bits), several 64-blocks per warp, every
@@ -663,7 +662,7 @@ __device__ bool sort_packed4096(int s0, int n, const SegSrc &src, int *pair_id, 
         }
         __syncthreads();
     }
-    return rank_ties_and_write<12>(pk, n, keys, ids, pair_id + s0);
+    return rank_ties_and_write<12>(pk, n, [keys](int i) { return keys[i]; }, ids, pair_id + s0);
 }
 
 __global__ void __launch_bounds__(256) k_tile_sort_small(const int *__restrict__ tile_start,
@@ -745,6 +744,106 @@ __global__ void __launch_bounds__(256) k_tile_sort_small(const int *__restrict__
     }
 }
 
+// Segments of 513 .. 4096 pairs in the direct (bucket) path -- every tile of the 10 M-sphere configuration: the
+// packed 32-bit sort with the float64 keys held in REGISTERS (<= 16 per thread) instead of a shared-memory
+// staging array.  Shared memory per CTA drops from 112 KB (sized for the 8192-pair fallback) to 32 KB (ids +
+// packed words), so four CTAs share an SM instead of two: the kernel waits on its random 8-byte key gathers and
+// on 78 block barriers, and both hide behind other CTAs.  The few words whose 20-bit key parts tie fetch their
+// full keys again for the exact ranking.  A segment with too many ties is left to k_tile_sort_big (its entry in
+// big_tiles stays positive); a sorted one is marked done (-1 - tile).
+__global__ void __launch_bounds__(256, 4) k_tile_sort_mid(const int *__restrict__ tile_start, int *pair_id,
+                                                          const int *__restrict__ bucket,
+                                                          const unsigned long long *__restrict__ key,
+                                                          const int *__restrict__ tile_cursor, int *big_tiles,
+                                                          const long long *__restrict__ status) {
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    int *ids = (int *)smem_raw;
+    unsigned *pk = (unsigned *)(smem_raw + (size_t)PACK_BIG * 4);
+    __shared__ unsigned long long s_lo[8], s_hi[8];
+    const long long flags = status[ST_FLAGS];
+    if (flags & (SS_FLAG_PAIR_OVERFLOW | SS_FLAG_LIST_FALLBACK)) return;
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const int n_big = big_tiles[0];
+    for (int bt = blockIdx.x; bt < n_big; bt += gridDim.x) {
+        const int t = big_tiles[1 + bt];
+        const int s0 = tile_start[t], n = tile_start[t + 1] - s0;
+        if (n > PACK_BIG) continue;
+        const int *bk = bucket + (size_t)t * BUCKET_CAP;
+        const int c_small = tile_cursor[t];
+        __syncthreads();  // previous segment's shared arrays fully consumed
+        unsigned long long kr[PACK_BIG / 256];
+        unsigned long long lo = ~0ull, hi = 0ull;
+#pragma unroll
+        for (int j = 0; j < PACK_BIG / 256; ++j) {
+            const int i = tid + 256 * j;
+            kr[j] = ~0ull;
+            if (i < n) {
+                const int id = bk[i < c_small ? i : BUCKET_CAP - 1 - (i - c_small)];
+                ids[i] = id;
+                kr[j] = key[id];
+            }
+        }
+#pragma unroll
+        for (int j = 0; j < PACK_BIG / 256; ++j)
+            if (tid + 256 * j < n) { lo = min(lo, kr[j]); hi = max(hi, kr[j]); }
+        for (int o = 16; o > 0; o >>= 1) {
+            lo = min(lo, __shfl_xor_sync(0xffffffffu, lo, o));
+            hi = max(hi, __shfl_xor_sync(0xffffffffu, hi, o));
+        }
+        if (lane == 0) { s_lo[warp] = lo; s_hi[warp] = hi; }
+        __syncthreads();
+#pragma unroll
+        for (int w = 0; w < 8; ++w) { lo = min(lo, s_lo[w]); hi = max(hi, s_hi[w]); }
+        const int bits = 64 - __clzll((long long)(hi - lo));
+        const int shift = bits > 20 ? bits - 20 : 0;
+        int np2 = 64;
+        while (np2 < n) np2 <<= 1;
+        const int n_blocks = np2 >> 6;
+#pragma unroll
+        for (int j = 0; j < PACK_BIG / 256; ++j) {
+            const int i = tid + 256 * j;
+            if (i < np2) pk[i] = i < n ? (((unsigned)((kr[j] - lo) >> shift) << 12) | (unsigned)i) : 0xffffffffu;
+        }
+        __syncthreads();
+        for (int b = warp; b < n_blocks; b += 8) {
+            const int i0 = (b << 6) + lane, i1 = i0 + 32;
+            unsigned e0 = pk[i0], e1 = pk[i1];
+            u_sort64(e0, e1, lane);
+            pk[i0] = e0; pk[i1] = e1;
+        }
+        __syncthreads();
+        const int half = np2 >> 1;
+        for (int k = 128; k <= np2; k <<= 1) {
+            const int hk = k >> 1;
+            for (int c = tid; c < half; c += blockDim.x) {  // flip
+                const int q = c & (hk - 1);
+                const int l = ((c - q) << 1) + q, r = ((c - q) << 1) + k - 1 - q;
+                const unsigned a = pk[l], b = pk[r];
+                if (b < a) { pk[l] = b; pk[r] = a; }
+            }
+            __syncthreads();
+            for (int j = hk >> 1; j >= 64; j >>= 1) {  // long-distance disperse stages
+                for (int c = tid; c < half; c += blockDim.x) {
+                    const int q = c & (j - 1);
+                    const int l = ((c - q) << 1) + q;
+                    const unsigned a = pk[l], b = pk[l + j];
+                    if (b < a) { pk[l] = b; pk[l + j] = a; }
+                }
+                __syncthreads();
+            }
+            for (int b = warp; b < n_blocks; b += 8) {  // j = 32 .. 1 in registers
+                const int i0 = (b << 6) + lane, i1 = i0 + 32;
+                unsigned e0 = pk[i0], e1 = pk[i1];
+                u_disperse64(e0, e1, lane);
+                pk[i0] = e0; pk[i1] = e1;
+            }
+            __syncthreads();
+        }
+        const bool ok = rank_ties_and_write<12>(pk, n, [key, ids](int i) { return key[ids[i]]; }, ids, pair_id + s0);
+        if (ok && tid == 0) big_tiles[1 + bt] = -1 - t;
+    }
+}
+
 // Persistent over the list of long segments (> SORT_SMALL pairs).  <= 4096: packed 32-bit sort, input from the tile's
 // bucket (or from the emitted pairs in the fallback path); <= SORT_BIG: 64-bit network in dynamic smem; longer: in
 // place in global memory.  Segments beyond 4096 only exist in the fallback path (they overflow the bucket).
@@ -764,6 +863,7 @@ __global__ void __launch_bounds__(256) k_tile_sort_big(const int *__restrict__ t
     int n_big = big_tiles[0];
     for (int b = blockIdx.x; b < n_big; b += gridDim.x) {
         int t = big_tiles[1 + b];
+        if (t < 0) continue;  // sorted by k_tile_sort_mid
         int s0 = tile_start[t], n = tile_start[t + 1] - s0;
         SegSrc src;
         src.direct = !(flags & SS_FLAG_LIST_FALLBACK);
@@ -853,6 +953,21 @@ cudaError_t launch_binning(const FwdLaunch &a, cudaStream_t s) {
             cudaError_t e = cudaFuncSetAttribute(k_tile_sort_big, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                                  (int)big_smem);
             if (e != cudaSuccess) return e;
+        }
+        {
+            static PerDeviceOnce mid_once;
+            const size_t mid_smem = (size_t)PACK_BIG * 8;
+            if (mid_once.first()) {
+                cudaError_t e = cudaFuncSetAttribute(k_tile_sort_mid, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                                     (int)mid_smem);
+                if (e != cudaSuccess) return e;
+            }
+            const int grid_mid = L.n_tiles < 148 * 4 ? L.n_tiles : 148 * 4;
+            ProfScope ps(KID_SORT_BIG, s);
+            k_tile_sort_mid<<<grid_mid, 256, mid_smem, s>>>(tile_start, pair_id, (const int *)(ws + L.bucket),
+                                                            (const unsigned long long *)(ws + L.key), tile_cursor,
+                                                            big_tiles, status);
+            count_launch();
         }
         int grid_big = L.n_tiles < 296 ? L.n_tiles : 296;
         {

@@ -320,10 +320,12 @@ __global__ void __launch_bounds__(TILE_PX, (KT <= 8 && DP <= 4) ? SS_RASTER_MINB
             zeta = t;
         }
         const float rf = mi.x;
-        const double rr = (double)rf * (double)rf;
-        const double hc2 = rr - dist2;
+        // r^2 - dist^2 in one rounding: r is a float32 value, so r * r is exact in float64 and the fused form
+        // equals the reference's (r * r) - dist2 bit for bit
+        const double rd = (double)rf;
+        const double hc2 = fma(rd, rd, -dist2);
         // dist2 < r^2 and t + half_chord > 0
-        if (hc2 > 0.0 && (t > 0.0 || t + sqrt(fmin(hc2, rr)) > 0.0)) {
+        if (hc2 > 0.0 && (t > 0.0 || t + sqrt(fmin(hc2, rd * rd)) > 0.0)) {
             ++n_hits;
             // float32 NDC depth for the blend exponent: (far - clip(zeta)) / (far - near)
             const float zeta_f = (MODE == SS_MODE_PINHOLE) ? (float)t * uzf : (float)t;
@@ -452,10 +454,7 @@ __global__ void __launch_bounds__(TILE_PX, (KT <= 8 && DP <= 4) ? SS_RASTER_MINB
 
         // float32 filter: every lane tests its pixel against a group of 32 relevant candidates and keeps the
         // outcome as one 32-bit word (candidate i of the group at bit 31 - i; the sign bit of d^2 - rho^2 is
-        // funnel-shifted in).  Two such words form the window; a lane always takes its oldest
-        // pending hit (highest set bit of the older word, else of the newer one), so lanes with few hits in the
-        // older group run ahead into the newer one while the busy lanes catch up, and the divergent float64
-        // path runs with most lanes active.
+        // funnel-shifted in).
         auto filter_group = [&](int g) -> unsigned {
             const int n = min(32, cnt - g);
             unsigned w = 0;
@@ -476,27 +475,33 @@ __global__ void __launch_bounds__(TILE_PX, (KT <= 8 && DP <= 4) ? SS_RASTER_MINB
             w &= 0xffffffffu << (32 - n);
             return w;
         };
-        unsigned w0 = 0, w1 = 0;  // older group, newer group (two 32-bit words: 64-bit shifts / tests cost double)
-        unsigned lpos = (unsigned)__cvta_generic_to_shared(lst);  // shared address of the older group's list entries
-        asm volatile("" : "+r"(lpos));
+        // Every lane owns two words: `wc`, the word it is draining, and `wn`, the word of the most recently filtered
+        // group (empty until the lane gets that far).  A lane whose current word runs empty takes over the next one,
+        // so lanes with few hits in a group run ahead by one group while the busy lanes catch up, and the divergent
+        // float64 path runs with most lanes active.  `bc - b` is the shared address of the list entry behind bit b
+        // of wc; `gl` is the same base for the newest group (warp-uniform).
+        unsigned wc, wn = 0u, bc;
+        unsigned gl = (unsigned)__cvta_generic_to_shared(lst) + 31u;
+        asm volatile("" : "+r"(gl));
         auto drain_round = [&]() {
-            const bool older = w0 != 0u;
-            const unsigned w = older ? w0 : w1;
-            if (w) {
-                const int b = 31 - __clz((int)w);  // highest set bit = oldest pending candidate (list entry 31 - b)
-                const unsigned bit = 1u << b;
-                if (older) w0 ^= bit; else w1 ^= bit;
-                process(lds_u8(lpos + (older ? 31 : 63) - b));
+            if (wc == 0u) { wc = wn; wn = 0u; bc = gl; }
+            if (wc) {
+                unsigned b;  // highest set bit = oldest pending candidate (list entry 31 - b)
+                asm("bfind.u32 %0, %1;" : "=r"(b) : "r"(wc));  // (31 - __clz costs two more integer instructions)
+                wc ^= 1u << b;
+                process(lds_u8(bc - b));
             }
         };
-        w0 = filter_group(0);
+        wc = filter_group(0);
+        bc = gl;
         for (int g = 32; g < cnt; g += 32) {
-            w1 = filter_group(g);
-            while (__any_sync(0xffffffffu, w0 != 0u)) drain_round();
-            w0 = w1; w1 = 0u;
-            lpos += 32;
+            const unsigned w = filter_group(g);
+            // the new word needs a free slot in every lane: drain until no lane holds two pending words
+            while (__any_sync(0xffffffffu, wn != 0u)) drain_round();
+            gl += 32u;
+            if (wc == 0u) { wc = w; bc = gl; } else wn = w;
         }
-        while (__any_sync(0xffffffffu, w0 != 0u)) drain_round();
+        while (__any_sync(0xffffffffu, (wc | wn) != 0u)) drain_round();
     }
 
     // finalise, raster.py:401-414

@@ -40,6 +40,7 @@ struct RasterArgs {
     // float32 depth used for the blend exponent and as a pre-filter of the top-K (the float64 depth is only
     // formed for hits that can enter the record): far, far - near, 1 / (far - near), error pad of the pre-filter
     float far_f, fmn_f, inv_range_f, zpad;
+    float ppu_f, ppu2_f;  // pixels per sensor unit and its square (the filter works in pixel units)
     int tau_on, store_buffer, collect_stats;
     float *image, *bg_weight;
     int *ids; float *z, *clos, *log_denom;
@@ -210,6 +211,7 @@ __global__ void __launch_bounds__(TILE_PX, (KT <= 8 && DP <= 4) ? SS_RASTER_MINB
     unsigned char *s_list = s_wmask + CAP;         // per warp: compacted indices of its relevant candidates
     constexpr int LSTRIDE = CAP + 4;
     __shared__ float4 s_rect[8];                   // per warp: sensor-space rectangle of its pixel centres
+    __shared__ float2 s_org[8];                    // per warp: sensor coordinates of its first pixel centre
     __shared__ double s_red[8];
     __shared__ unsigned long long s_stat[3];
 
@@ -233,14 +235,7 @@ __global__ void __launch_bounds__(TILE_PX, (KT <= 8 && DP <= 4) ? SS_RASTER_MINB
         double vn = sqrt(xs * xs + ys * ys + cam.focal * cam.focal);
         ux = xs / vn; uy = ys / vn; uz = cam.focal / vn;
     }
-    // float32 sensor coordinates for the screen-space filter; an out-of-image (or finished) pixel
-    // gets a NaN coordinate so it never passes (arithmetic NaNs are canonical 0x7fffffff: sign bit
-    // clear, also against an infinite rho^2, where a huge finite coordinate would still pass)
-    const float kFar = __int_as_float(0x7fffffff);
     const float uzf = (float)uz;
-    float fx = valid ? (float)xs : kFar;
-    float fy = (float)ys;
-    fx = pin_reg(fx); fy = pin_reg(fy);
     {   // sensor-space rectangle spanned by this warp's in-image pixel centres (empty: +inf/-inf)
         float x0 = valid ? (float)xs : INFINITY, x1 = valid ? (float)xs : -INFINITY;
         float y0 = valid ? (float)ys : INFINITY, y1 = valid ? (float)ys : -INFINITY;
@@ -248,7 +243,11 @@ __global__ void __launch_bounds__(TILE_PX, (KT <= 8 && DP <= 4) ? SS_RASTER_MINB
             x0 = fminf(x0, __shfl_xor_sync(0xffffffffu, x0, o)); x1 = fmaxf(x1, __shfl_xor_sync(0xffffffffu, x1, o));
             y0 = fminf(y0, __shfl_xor_sync(0xffffffffu, y0, o)); y1 = fmaxf(y1, __shfl_xor_sync(0xffffffffu, y1, o));
         }
-        if (lane == 0) s_rect[warp] = make_float4(x0, x1, y0, y1);
+        if (lane == 0) {
+            s_rect[warp] = make_float4(x0, x1, y0, y1);
+            s_org[warp] = make_float2((float)xs, (float)ys);  // pixel centre of the block's column 0, row 0
+        }
+        __syncwarp();
     }
 
     const bool overflow = (a.status[ST_FLAGS] & SS_FLAG_PAIR_OVERFLOW) != 0;  // lists not built
@@ -431,8 +430,7 @@ __global__ void __launch_bounds__(TILE_PX, (KT <= 8 && DP <= 4) ? SS_RASTER_MINB
             const double zb = (far_ - fmin(fmax(e0 * tile_cos, near_), far_)) * inv_range;
             const double z_stop = a.gamma * (a.log_tau + (double)((m2 + log2f(denom)) * kLn2));
             if (!done && zb < z_stop) {
-                done = true;
-                fx = pin_reg(kFar);  // a finished pixel ignores later hits (raster.py:375-376)
+                done = true;  // a finished pixel ignores later hits (raster.py:375-376): its filter words are masked
             }
             if (__syncthreads_and(done)) break;
         }
@@ -452,28 +450,51 @@ __global__ void __launch_bounds__(TILE_PX, (KT <= 8 && DP <= 4) ? SS_RASTER_MINB
         if (lane < 4) lst[cnt + lane] = 0;  // padding of the last group of 4: a readable slot, masked out below
         __syncwarp();
 
-        // float32 filter: every lane tests its pixel against a group of 32 relevant candidates and keeps the
-        // outcome as one 32-bit word (candidate i of the group at bit 31 - i; the sign bit of d^2 - rho^2 is
-        // funnel-shifted in).
+        // float32 filter, candidate-parallel: lane l takes candidate 31 - l of a group of 32 relevant candidates and
+        // builds the 32-bit mask of the block's pixels (bit p = row p / 8, column p % 8) that lie inside the
+        // candidate's bounding circle, row by row from the circle's x-extent on that row; a 32 x 32 bit transpose by
+        // shuffles then hands every lane the word of ITS pixel (candidate i at bit 31 - i).  ~3.6 instructions per
+        // candidate and warp instead of the 8 of a per-pixel test of every candidate.  The mask is a superset of
+        // the per-pixel test dx^2 + dy^2 < rho^2 (rho^2 widened by 0.1 % + 0.01 px^2, column ranges rounded outwards
+        // by 0.002 px); the float64 evaluation in process() decides every hit, so a superset only costs a round.
+        const float2 org = s_org[warp];
         auto filter_group = [&](int g) -> unsigned {
             const int n = min(32, cnt - g);
-            unsigned w = 0;
-            int k = 0;
-#pragma unroll 2
-            for (; k < n; k += 4) {
-                const unsigned idx4 = *reinterpret_cast<const unsigned *>(lst + g + k);
+            const int i = 31 - lane;
+            unsigned x = 0u;
+            if (i < n) {
+                const float4 c = s_cf[lst[g + i]];
+                const float cxp = (c.x - org.x) * a.ppu_f;  // centre in pixel units relative to the block's first pixel
+                const float cyp = (c.y - org.y) * a.ppu_f;
+                float r2p = c.z * a.ppu2_f;
+                r2p = fmaf(r2p, 1e-3f, r2p) + 1e-2f;
+                const float lo_a = cxp + 0.498f, hi_a = cxp - 0.498f;  // ceil(v) ~ rne(v + 0.498), floor(v) ~ rne(v - 0.498)
+                constexpr float kMagic = 12582912.0f;  // 1.5 * 2^23: (v + kMagic) holds rne(v) in its low mantissa bits
 #pragma unroll
-                for (int u = 0; u < 4; ++u) {
-                    const float4 c = s_cf[(idx4 >> (8 * u)) & 0xffu];
-                    const float dx = fx - c.x, dy = fy - c.y;
-                    const float sgn = fmaf(dx, dx, fmaf(dy, dy, -c.z));  // negative = inside the bounding circle
-                    w = __funnelshift_l(__float_as_uint(sgn), w, 1);
+                for (int r = 0; r < 4; ++r) {
+                    const float dy = (float)r - cyp;
+                    float hw;  // half-width of the circle on this row; NaN when the row misses it
+                    asm("sqrt.approx.ftz.f32 %0, %1;" : "=f"(hw) : "f"(fmaf(-dy, dy, r2p)));
+                    // first / last column inside, clamped so that an empty row gives lo > hi (fmaxf drops the NaN)
+                    const float lo_f = fminf(fmaxf(lo_a - hw, -0.4f), 8.4f);
+                    const float hi_f = fminf(fmaxf(hi_a + hw, -1.4f), 7.4f);
+                    const unsigned sl = __float_as_uint(lo_f + (kMagic + 8.0f * r)) & 63u;           // 8 r + lo: 0 .. 32
+                    const unsigned sr = __float_as_uint((kMagic + 31.0f - 8.0f * r) - hi_f) & 63u;   // 31 - (8 r + hi): 0 .. 32
+                    unsigned ml, mr;  // shifts by 32 must give 0: PTX shl / shr clamp the amount
+                    asm("shl.b32 %0, %1, %2;" : "=r"(ml) : "r"(0xffffffffu), "r"(sl));
+                    asm("shr.u32 %0, %1, %2;" : "=r"(mr) : "r"(0xffffffffu), "r"(sr));
+                    x |= ml & mr & (0xffu << (8 * r));
                 }
             }
-            // k = n rounded up to 4: candidate i sits at bit k - 1 - i; left-align and drop the padding
-            w <<= (32 - k);
-            w &= 0xffffffffu << (32 - n);
-            return w;
+            // bit-matrix transpose: x[lane l] bit p  ->  x[lane p] bit l
+#pragma unroll
+            for (int j = 16; j > 0; j >>= 1) {
+                const unsigned m = j == 16 ? 0x0000ffffu : j == 8 ? 0x00ff00ffu : j == 4 ? 0x0f0f0f0fu
+                                                        : j == 2 ? 0x33333333u : 0x55555555u;
+                const unsigned t = __shfl_xor_sync(0xffffffffu, x, j);
+                x = (lane & j) ? (((t >> j) & m) | (x & ~m)) : ((x & m) | ((t << j) & ~m));
+            }
+            return done ? 0u : x;
         };
         // Every lane owns two words: `wc`, the word it is draining, and `wn`, the word of the most recently filtered
         // group (empty until the lane gets that far).  A lane whose current word runs empty takes over the next one,
@@ -614,6 +635,8 @@ cudaError_t launch_raster(const FwdLaunch &a, cudaStream_t s, int tile0, int n_t
     r.far_f = (float)a.cam.far_;
     r.fmn_f = (float)(a.cam.far_ - a.cam.near_);
     r.inv_range_f = (float)a.cam.inv_range;
+    r.ppu_f = (float)a.cam.ppu;
+    r.ppu2_f = (float)(a.cam.ppu * a.cam.ppu);
     // |float32 depth - float64 depth| <= ~6 roundings of (|far| + |zeta|) / (far - near); padded 4x
     r.zpad = (float)(24.0 * ldexp(1.0, -24) * (fabs(a.cam.far_) + fabs(a.cam.near_) + (a.cam.far_ - a.cam.near_)) *
                      a.cam.inv_range);

@@ -540,6 +540,10 @@ __global__ void __launch_bounds__(256) k_finalize(FinArgs a) {
             if (blk + gridDim.x < n_blocks && inext < a.M) {
                 const float4 *rown = (const float4 *)(a.raw + (size_t)inext * RS);
                 n0 = rown[0]; n1 = rown[1];
+                // a touched sphere also needs its projected radius and position: the kernel spent half its warp time
+                // waiting for those two dependent loads (ncu long-scoreboard samples); request the lines now
+                if (a.normalize || a.gate) asm volatile("prefetch.global.L1 [%0];" ::"l"(a.proj_r + inext));
+                if (a.cam_grads) asm volatile("prefetch.global.L1 [%0];" ::"l"(a.pos + 3 * inext));
             }
         }
         if (i >= a.M) continue;
@@ -723,7 +727,7 @@ cudaError_t launch_backward(const BwdLaunch &a, cudaStream_t s) {
     {
         ProfScope ps(KID_MEMSET_BWD, s);
         const size_t n4 = (size_t)M * L.raw_stride / 4;
-        k_raw_prepare<<<148 * 8, 256, 0, s>>>((float4 *)raw, n4, bst, tag);
+        k_raw_prepare<<<148, 256, 0, s>>>((float4 *)raw, n4, bst, tag);  // (grid-stride; usually one block's worth of work)
         count_launch();
     }
     BackArgs b;

@@ -935,7 +935,7 @@ cudaError_t launch_binning(const FwdLaunch &a, cudaStream_t s) {
     count_launch();
     if (M > 0) {
         unsigned grid = (unsigned)((M + 255) / 256);
-        if (grid > 148 * 4) grid = 148 * 4;  // grid-stride: in the usual (bucket) case the launch is an early exit
+        if (grid > 148) grid = 148;  // grid-stride: in the usual (bucket) case the launch is an early exit
         {
             ProfScope ps(KID_EMIT, s);
             k_emit<<<grid, 256, 0, s>>>(M, (const ushort4 *)(ws + L.trect), (const int4 *)(ws + L.slot4),

@@ -11,6 +11,14 @@ ncu --metrics gpu__time_duration.sum --clock-control none -c 400 --csv --log-fil
     python bench.py --steps 3 --warmup 3 --no-cpu-baseline > $out/${tag}_launches_bench.log 2>&1
 ncu --set full --clock-control none --import-source on -k regex:'k_' -s 11 -c 11 -o $out/${tag}_full \
     python scripts/quick_time.py > $out/${tag}_full.log 2>&1
+# tracked exports of the capture: every raw metric per kernel, the compact per-kernel table + the JSON bench.py
+# reads (profiles/ncu_kernels.json), and the per-source-line instruction / stall table of the raster kernel
+ncu -i $out/${tag}_full.ncu-rep --page raw --csv > $out/${tag}_ncu_raw_all_metrics.csv 2>/dev/null
+python scripts/ncu_extract.py $out/${tag}_ncu_raw_all_metrics.csv $out/${tag}_kernels.csv $out/${tag}_ncu_kernels.json > /dev/null
+ncu -i $out/${tag}_full.ncu-rep --page source --csv --print-source cuda,sass > $out/${tag}_src.csv 2>/dev/null
+python scripts/ncu_stalls.py $out/${tag}_src.csv k_raster 45 > $out/${tag}_raster_stalls.txt 2>&1
+python scripts/launch_shares.py $out/${tag}_launches.csv > $out/${tag}_launch_shares.txt 2>&1
+python scripts/run_config.py --count 10000000 --width 1920 --height 1080 --d 16 --k 32 --tau 0.01 > $out/${tag}_c5.log 2>&1
 SAN="tests/test_gpu_parity.py::test_golden_forward tests/test_gpu_parity.py::test_golden_backward tests/test_gpu_fuzz.py tests/test_gpu_api.py::test_early_stop_bound_and_chunk_sizes"
 compute-sanitizer --tool memcheck --error-exitcode 1 python -m pytest $SAN -x -q > $out/${tag}_sanitizer_memcheck.log 2>&1
 compute-sanitizer --tool racecheck --error-exitcode 1 python -m pytest tests/test_gpu_parity.py::test_golden_forward tests/test_gpu_parity.py::test_golden_backward -x -q > $out/${tag}_sanitizer_racecheck.log 2>&1

@@ -168,14 +168,16 @@ class RenderEngine:
     # -- forward ---------------------------------------------------------------------
     def forward(self, pos, rad, opa, feat, bg, cam: CameraSpec, gamma=0.1, eps=1e-2, tau=0.01, top_k=5,
                 chunk=256, tile=16, store_buffer=True, collect_stats=False, validate=True,
-                check=True, debug=False, image=None, bg_weight=None, band_events=None):
+                check=True, debug=False, image=None, bg_weight=None, band_events=None, after_launch=None):
         """Enqueue the forward pipeline.  Inputs: float32 CUDA tensors (or array-likes, which are
         copied to the device).  Returns a dict of CUDA tensors; with check=True the status block
         is read back (one stream sync), validation / overflow are handled and `status` is set.
 
         band_events: a list of torch.cuda.Event -- the image is then drawn in that many bands of tile rows
         (ss_forward_banded) and event b is recorded when the rows `band_rows(height, n, b)` are final, so that a
-        copy stream can download the upper bands while the lower ones are still being drawn."""
+        copy stream can download the upper bands while the lower ones are still being drawn.  after_launch: called
+        right after the kernels have been enqueued, i.e. before a check=True status read synchronises the stream
+        (the place to enqueue such downloads; called again if an overflow makes the engine render a second time)."""
         dev = self.device
         bg = _dev_f32(bg, dev, (-1,))
         d = bg.shape[0]
@@ -241,6 +243,8 @@ class RenderEngine:
                     rc = self.lib.ss_forward(C.byref(a), self._stream())
             if rc != _lib.SS_OK:
                 _raise_for(rc)
+            if after_launch is not None:
+                after_launch()
             if not check:
                 break
             status = self.read_status()

@@ -32,6 +32,36 @@ GATE_RADIUS_PX = 3.0
 _IMAGE_BANDS = 4
 
 
+def _reference_of(obj):
+    """The reference package itself when `obj` (a scene) is one of ITS objects, else None.  A caller that hands in
+    the reference's types -- its fit loop with this renderer plugged in, its own test files -- gets the reference's
+    artefact types back (its shading and loss code check `isinstance(image, FeatureImage)`, shade.py:19-22) and
+    the reference's exception classes raised (`pytest.raises(ContractViolation)` in tests/test_grad.py)."""
+    import sys
+    if type(obj).__module__.split(".")[0] != "softsphere":
+        return None
+    ref = sys.modules.get("softsphere")
+    return ref if ref is not None and hasattr(ref, "raster") and hasattr(ref, "grad") else None
+
+
+def _raises_reference_errors(fn):
+    """Re-raises this package's exceptions as the same-named classes of the reference (errors.py:4-25) when the
+    scene argument is a reference object."""
+    import functools
+
+    @functools.wraps(fn)
+    def wrapper(scene, *args, **kwargs):
+        try:
+            return fn(scene, *args, **kwargs)
+        except Exception as e:  # noqa: BLE001
+            ref = _reference_of(scene)
+            cls = getattr(getattr(ref, "errors", None), type(e).__name__, None) if ref is not None else None
+            if cls is None or isinstance(e, cls) or type(e).__module__.split(".")[0] != __name__.split(".")[0]:
+                raise
+            raise cls(*e.args) from e
+    return wrapper
+
+
 def _scene_columns(scene):
     m = len(scene)
     d = int(scene.feature_dim)
@@ -145,6 +175,7 @@ def _download_widened(eng: RenderEngine, pieces):
     return out
 
 
+@_raises_reference_errors
 def render_forward(scene, camera, params, *, workers: int = 1, dtype=np.float64,
                    tile_size: int = DEFAULT_TILE_SIZE, store_buffer: bool = True, chunk_size: int = 256,
                    engine: RenderEngine = None):
@@ -221,9 +252,13 @@ def render_forward(scene, camera, params, *, workers: int = 1, dtype=np.float64,
         on = res["on_sensor"].cpu().numpy().astype(bool)
         pairs = (rect[:, 1] // ts - rect[:, 0] // ts + 1) * (rect[:, 3] // ts - rect[:, 2] // ts + 1)
         tested = int(pairs[on].sum())
-    stats = RenderStats(spheres_total=len(scene), spheres_on_sensor=stat["spheres_on_sensor"],
-                        candidates_tested=tested, hits_blended=stat["hits_blended"],
-                        pixels_early_stopped=stat["pixels_early_stopped"], tiles=ntx * nty)
+    ref = _reference_of(scene)
+    stats_cls = ref.raster.RenderStats if ref is not None else RenderStats
+    stats = stats_cls(spheres_total=len(scene), spheres_on_sensor=stat["spheres_on_sensor"],
+                      candidates_tested=tested, hits_blended=stat["hits_blended"],
+                      pixels_early_stopped=stat["pixels_early_stopped"], tiles=ntx * nty)
+    if ref is not None:  # (the buffer stays this package's lazily downloaded record: it is duck-typed everywhere)
+        image = ref.raster.FeatureImage(data=image.data, background_weight=image.background_weight)
     return image, buffer, stats
 
 
@@ -254,6 +289,7 @@ def _device_record(buffer, device):
             "log_denom": up(buffer.log_denom, np.float32)}
 
 
+@_raises_reference_errors
 def render_backward(scene, camera, params, buffer: BackwardBuffer, upstream, *, workers: int = 1,
                     normalize: bool = True, gate: bool = True, tile_size: int = 16,
                     engine: RenderEngine = None, reuse_upload: bool = True, deterministic: bool = False):
@@ -301,6 +337,13 @@ def render_backward(scene, camera, params, buffer: BackwardBuffer, upstream, *, 
         d_rot = rotation_6d_vjp(camera.rotation_param, g_rot)
     cam_grads = CameraGradients(d_translation=cg[0:3].copy(), d_rotation=d_rot, d_focal=float(cg[12]),
                                 d_sensor_width=float(cg[13]))
+    ref = _reference_of(scene)
+    if ref is not None:
+        grads = ref.grad.SceneGradients(d_position=grads.d_position, d_radius=grads.d_radius,
+                                        d_opacity=grads.d_opacity, d_feature=grads.d_feature,
+                                        pixel_count=grads.pixel_count)
+        cam_grads = ref.grad.CameraGradients(d_translation=cam_grads.d_translation, d_rotation=cam_grads.d_rotation,
+                                             d_focal=cam_grads.d_focal, d_sensor_width=cam_grads.d_sensor_width)
     return grads, cam_grads
 
 

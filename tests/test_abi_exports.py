@@ -86,3 +86,31 @@ def test_workspace_bytes_and_argument_checks(lib):
     assert lib.ss_forward(C.byref(a), None) == _lib.SS_ERR_CAMERA
     a.cam.far_ = 45.0
     assert lib.ss_forward(C.byref(a), None) == _lib.SS_ERR_NULL  # no buffers given
+
+
+def test_banded_forward_argument_checks_and_band_rows(lib):
+    """ss_forward_banded / ss_band_rows: host-side checks and the band geometry (no CUDA call is reached)."""
+    a = _lib.SsForwardArgs()
+    a.dims = _lib.SsDims(0, 16, 3, 32, 32, 5)
+    a.cam.width, a.cam.height, a.cam.focal, a.cam.sensor_w, a.cam.near_, a.cam.far_ = 32, 32, 5.0, 2.0, 0.1, 45.0
+    a.blend = _lib.SsBlend(0.1, 0.01, 0.0, 16, 256, 0, 0)
+    ev = (C.c_void_p * 2)(C.c_void_p(1), C.c_void_p(2))
+    assert lib.ss_forward_banded(C.byref(a), 0, ev, None) == _lib.SS_ERR_PARAMS
+    assert lib.ss_forward_banded(C.byref(a), 17, ev, None) == _lib.SS_ERR_PARAMS  # SS_MAX_BANDS = 16
+    assert lib.ss_forward_banded(C.byref(a), 2, None, None) == _lib.SS_ERR_NULL
+    missing = (C.c_void_p * 2)(C.c_void_p(1), C.c_void_p(None))
+    assert lib.ss_forward_banded(C.byref(a), 2, missing, None) == _lib.SS_ERR_NULL
+    assert lib.ss_forward_banded(C.byref(a), 2, ev, None) == _lib.SS_ERR_NULL  # (no buffers given, like ss_forward)
+    r0, r1 = C.c_int(), C.c_int()
+    # bands are whole tile rows, contiguous, top to bottom, and cover the image: 1080 rows = 68 tile rows
+    for height, n in ((1080, 4), (100, 3), (16, 16), (1, 1), (1024, 2)):
+        prev = 0
+        for b in range(n):
+            assert lib.ss_band_rows(height, n, b, C.byref(r0), C.byref(r1)) == _lib.SS_OK
+            assert r0.value == prev and r0.value <= r1.value <= height
+            assert r0.value % 16 == 0 or r0.value == height
+            prev = r1.value
+        assert prev == height
+    assert lib.ss_band_rows(64, 2, 2, C.byref(r0), C.byref(r1)) == _lib.SS_ERR_PARAMS
+    assert lib.ss_band_rows(64, 0, 0, C.byref(r0), C.byref(r1)) == _lib.SS_ERR_PARAMS
+    assert lib.ss_band_rows(64, 2, 0, None, C.byref(r1)) == _lib.SS_ERR_NULL

@@ -210,3 +210,26 @@ def test_reference_acceptance_checks_through_the_adapter(engine, ref):
     grad_close(mixed.d_position, want.d_position, "adapter backward on the reference's buffer")
     grad_close(mixed.d_feature, want.d_feature, "adapter backward on the reference's buffer (features)")
     grad_close(mixed_c.d_translation, want_c.d_translation, "adapter backward on the reference's buffer (camera)")
+
+
+def test_plugin_forward_survives_a_workspace_regrowth():
+    """render_forward downloads the image band by band from a hook that runs before the status read; when the
+    pair capacity overflows, the engine regrows its workspace and renders again (the hook runs a second time):
+    the image that comes back must be the second, complete one."""
+    import paper_2004_07484_b200 as pk
+    from oracle import oracle as orc
+    eng = pk.RenderEngine("cuda", pair_factor=1.0, min_pairs=8)
+    pos = np.array([[0, 0, 3.0], [0.5, 0.2, 20.0], [0, 0, 10.0]], np.float32)
+    rad = np.array([2.9, 1.0, 30.0], np.float32)  # third: camera inside the sphere -> every tile
+    opa = np.array([0.6, 0.9, 0.3], np.float32)
+    feat, bg = np.eye(3, dtype=np.float32), np.zeros(3, np.float32)
+    vec = [0, 0, 0, 0, 0, 0, 5.0, 2.0]
+    scene = _scene_obj(pk, pos, rad, opa, feat, bg)
+    cam = pk.camera_from_vector(vec, 72, 100)  # 7 tile rows: uneven bands
+    params = pk.BlendParams(gamma=0.2, epsilon=1e-2, tau=0.0, top_k=5)
+    image, buffer, stats = pk.render_forward(scene, cam, params, engine=eng)
+    ref = orc.render_forward(pos, rad, opa, feat, bg, orc.camera_from_vector(vec, 72, 100), gamma=0.2, tau=0.0)
+    assert stats.candidates_tested == ref["stats"]["candidates_tested"] > 8
+    assert_close(image.data, ref["image"], FWD_RTOL, FWD_ATOL, "image after regrowth")
+    assert_close(image.background_weight, ref["bg_weight"], FWD_RTOL, FWD_ATOL, "bg_weight after regrowth")
+    assert np.array_equal(buffer.ids, ref["ids"])

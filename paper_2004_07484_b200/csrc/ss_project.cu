@@ -537,26 +537,36 @@ __device__ bool rank_ties_and_write(const unsigned *pk, int n, KeyFn keys, const
 // pk: 512 words.  Returns false (nothing written) when too many packed words tie.
 __device__ bool sort_packed512(int s0, int n, int np2, const SegSrc &src, int *pair_id,
                                unsigned long long *keys, int *ids, unsigned *pk) {
-    __shared__ unsigned long long s_min[8], s_max[8];
+    // The key range is taken from the UPPER words of the keys only (sign, exponent and 20 mantissa bits of the
+    // depth): lo = min upper word << 32 <= every key, range = (max upper word : ffffffff) - lo >= the true range.
+    // The map stays monotone, and it is the same map whenever the depths of a tile differ in their upper words --
+    // always, except for near-equal depths, whose words then tie and take the exact ranking below.  A 32-bit
+    // min / max costs a quarter of the instructions of the 64-bit one (10 % of this kernel).
+    __shared__ unsigned s_min[8], s_max[8];
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const int n_blocks = np2 >> 6;  // <= 8: at most one 64-block per warp
     const int i0 = (warp << 6) + lane, i1 = i0 + 32;
-    unsigned long long k0 = ~0ull, k1 = ~0ull, lo = ~0ull, hi = 0ull;
+    unsigned long long k0 = ~0ull, k1 = ~0ull;
+    unsigned lo32 = 0xffffffffu, hi32 = 0u;
     if (warp < n_blocks) {
         int id0, id1;
-        if (i0 < n) { src.load(i0, k0, id0); keys[i0] = k0; ids[i0] = id0; lo = k0; hi = k0; }
-        if (i1 < n) { src.load(i1, k1, id1); keys[i1] = k1; ids[i1] = id1; lo = min(lo, k1); hi = max(hi, k1); }
+        if (i0 < n) { src.load(i0, k0, id0); keys[i0] = k0; ids[i0] = id0; lo32 = hi32 = (unsigned)(k0 >> 32); }
+        if (i1 < n) {
+            src.load(i1, k1, id1); keys[i1] = k1; ids[i1] = id1;
+            lo32 = min(lo32, (unsigned)(k1 >> 32)); hi32 = max(hi32, (unsigned)(k1 >> 32));
+        }
     }
     for (int o = 16; o > 0; o >>= 1) {
-        lo = min(lo, __shfl_xor_sync(0xffffffffu, lo, o));
-        hi = max(hi, __shfl_xor_sync(0xffffffffu, hi, o));
+        lo32 = min(lo32, __shfl_xor_sync(0xffffffffu, lo32, o));
+        hi32 = max(hi32, __shfl_xor_sync(0xffffffffu, hi32, o));
     }
-    if (lane == 0) { s_min[warp] = lo; s_max[warp] = hi; }
+    if (lane == 0) { s_min[warp] = lo32; s_max[warp] = hi32; }
     __syncthreads();
 #pragma unroll
-    for (int w = 0; w < 8; ++w) { lo = min(lo, s_min[w]); hi = max(hi, s_max[w]); }
-    const unsigned long long range = hi - lo;
-    const int bits = 64 - __clzll((long long)range);  // 0 when every key is equal
+    for (int w = 0; w < 8; ++w) { lo32 = min(lo32, s_min[w]); hi32 = max(hi32, s_max[w]); }
+    const unsigned long long lo = (unsigned long long)lo32 << 32;
+    const unsigned long long range = (((unsigned long long)hi32 << 32) | 0xffffffffull) - lo;
+    const int bits = 64 - __clzll((long long)range);  // >= 32
     const int shift = bits > 23 ? bits - 23 : 0;
     unsigned e0 = 0xffffffffu, e1 = 0xffffffffu;  // padding sorts last
     if (warp < n_blocks) {

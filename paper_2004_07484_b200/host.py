@@ -158,13 +158,11 @@ class HostRenderSession:
         # two image buffers, alternating by view: the download of view i must not hold back the forward of view i + 1
         self._images = [torch.empty((h, w, d), dtype=f32, device=dev) for _ in range(2)]
         self._image_copied = [torch.cuda.Event(), torch.cuda.Event()]
-        self.bg_weight = torch.empty((h, w), dtype=f32, device=dev)
-        self.ids = torch.empty((k, h, w), dtype=torch.int32, device=dev)
-        self.z = torch.empty((k, h, w), dtype=f32, device=dev)
-        self.closeness = torch.empty((k, h, w), dtype=f32, device=dev)
-        self.log_denom = torch.empty((h, w), dtype=f32, device=dev)
-        self._prep_key = None
-        self._fa = self._ba = None
+        # "lane" j = an engine (workspace) + its forward outputs + its upstream buffer + its argument blocks.  Lane 0
+        # serves single views; multi-view steps alternate views between lane 0 and lane 1 (allocated on first use)
+        # on two compute streams, so the forward of view i + 1 runs under the backward of view i.
+        self._lanes = [self._new_lane(self.engine, self.upstream)]
+        self._compute_streams = None
 
         self.packed = PackedGradients(m, d, dev)
         self.out, self.h_grads = self.packed.dev, self.packed.host
@@ -178,61 +176,135 @@ class HostRenderSession:
         self.last_h2d_bytes = 0
         self.last_d2h_bytes = 0
 
-    def _prepared(self):
-        """Argument blocks of ss_forward / ss_backward with every pointer filled in; rebuilt only when the engine's
-        workspace moved or was re-laid out (the engine may be shared with other callers)."""
-        eng = self.engine
+    def _new_lane(self, engine, upstream):
+        dev, f32 = engine.device, torch.float32
+        h, w, k = self.h, self.w, self.k
+        return {"engine": engine, "upstream": upstream, "key": None, "fa": None, "ba": None, "events_c": None,
+                "bg_weight": torch.empty((h, w), dtype=f32, device=dev),
+                "ids": torch.empty((k, h, w), dtype=torch.int32, device=dev),
+                "z": torch.empty((k, h, w), dtype=f32, device=dev),
+                "closeness": torch.empty((k, h, w), dtype=f32, device=dev),
+                "log_denom": torch.empty((h, w), dtype=f32, device=dev)}
+
+    def _lane(self, j):
+        while len(self._lanes) <= j:
+            e = self.engine
+            twin = RenderEngine(e.device, pair_factor=e.pair_factor, min_pairs=e.min_pairs)
+            self._lanes.append(self._new_lane(twin, torch.empty_like(self.upstream)))
+        return self._lanes[j]
+
+    def _prepared(self, lane):
+        """Argument blocks of ss_forward / ss_backward with every pointer filled in; rebuilt only when the lane's
+        workspace moved or was re-laid out (the first lane's engine may be shared with other callers)."""
+        eng = lane["engine"]
         dims = eng._ensure_workspace(self.m, self.d, self.w, self.h, self.k)
         key = (eng._ws.data_ptr(), eng._ws.numel(), int(dims.max_pairs))
-        if key != self._prep_key:
+        if key != lane["key"]:
             fa, ba = _lib.SsForwardArgs(), _lib.SsBackwardArgs()
             for a in (fa, ba):
                 a.dims = dims
                 a.pos, a.rad, a.opa, a.feat, a.bg = (_ptr(self.pos), _ptr(self.rad), _ptr(self.opa), _ptr(self.feat),
                                                      _ptr(self.bg))
                 a.workspace, a.workspace_bytes = _ptr(eng._ws), eng._ws.numel()
-                a.ids, a.z, a.closeness, a.log_denom = (_ptr(self.ids), _ptr(self.z), _ptr(self.closeness),
-                                                        _ptr(self.log_denom))
-            fa.bg_weight = _ptr(self.bg_weight)
-            ba.upstream = _ptr(self.upstream)
+                a.ids, a.z, a.closeness, a.log_denom = (_ptr(lane["ids"]), _ptr(lane["z"]), _ptr(lane["closeness"]),
+                                                        _ptr(lane["log_denom"]))
+            fa.bg_weight = _ptr(lane["bg_weight"])
+            ba.upstream = _ptr(lane["upstream"])
             o = self.out
             ba.d_pos, ba.d_rad, ba.d_opa, ba.d_feat = _ptr(o["d_pos"]), _ptr(o["d_rad"]), _ptr(o["d_opa"]), _ptr(o["d_feat"])
             ba.pixel_count, ba.cam_grad = _ptr(o["pixel_count"]), _ptr(o["cam_grad"])
-            self._fa, self._ba, self._prep_key = fa, ba, key
-            self._events_c = None
-        return self._fa, self._ba
+            lane["fa"], lane["ba"], lane["key"], lane["events_c"] = fa, ba, key, None
+        return lane["fa"], lane["ba"]
 
-    def _forward_fast(self, cam, gamma, eps, tau, events, stream, image):
+    def _forward_fast(self, cam, gamma, eps, tau, events, stream, image, lane=None):
         """ss_forward[_banded] on the session's own buffers without the engine's per-call checks and allocations
         (no status read: the caller polls engine.read_status(), like engine.forward(check=False))."""
-        fa, _ = self._prepared()
+        lane = lane or self._lanes[0]
+        fa, _ = self._prepared(lane)
         fa.cam, fa.image = cam.to_c(), _ptr(image)
         fa.blend = _lib.SsBlend(float(gamma), float(eps), float(tau), 16, 256, _lib.OPT_STORE_BUFFER, 0)
-        lib, sp = self.engine.lib, C.c_void_p(stream.cuda_stream)
+        lib, sp = lane["engine"].lib, C.c_void_p(stream.cuda_stream)
         if events:
-            if self._events_c is None or len(self._events_c) != len(events):
+            if lane["events_c"] is None or len(lane["events_c"]) != len(events):
                 for e in events:  # a torch event only gets its CUDA handle on first record
                     if not e.cuda_event:
                         e.record(stream)
-                self._events_c = (C.c_void_p * len(events))(*[C.c_void_p(e.cuda_event) for e in events])
-            rc = lib.ss_forward_banded(C.byref(fa), len(events), self._events_c, sp)
+                lane["events_c"] = (C.c_void_p * len(events))(*[C.c_void_p(e.cuda_event) for e in events])
+            rc = lib.ss_forward_banded(C.byref(fa), len(events), lane["events_c"], sp)
         else:
             rc = lib.ss_forward(C.byref(fa), sp)
         if rc != _lib.SS_OK:
             _raise_for(rc)
-        self.engine._last_fwd = None  # (the engine's own record-reuse bookkeeping does not cover this call)
+        lane["engine"]._last_fwd = None  # (the engine's own record-reuse bookkeeping does not cover this call)
 
-    def _backward_fast(self, cam, gamma, eps, normalize, gate, accumulate, stream):
-        _, ba = self._prepared()
+    def _backward_fast(self, cam, gamma, eps, normalize, gate, accumulate, stream, lane=None):
+        lane = lane or self._lanes[0]
+        _, ba = self._prepared(lane)
         ba.cam = cam.to_c()
         # the draw records in the workspace are those of the forward call just made on the same, untouched inputs
         flags = _lib.OPT_CAMERA_GRADS | _lib.OPT_REUSE_RECORDS
         flags |= (_lib.OPT_NORMALIZE if normalize else 0) | (_lib.OPT_GATE if gate else 0)
         flags |= _lib.OPT_ACCUMULATE if accumulate else 0
         ba.blend = _lib.SsBlend(float(gamma), float(eps), 0.0, 16, 256, flags, 0)
-        rc = self.engine.lib.ss_backward(C.byref(ba), C.c_void_p(stream.cuda_stream))
+        rc = lane["engine"].lib.ss_backward(C.byref(ba), C.c_void_p(stream.cuda_stream))
         if rc != _lib.SS_OK:
             _raise_for(rc)
+
+    def _views_pipelined(self, cams, gamma, eps, tau, normalize, gate, main):
+        """Multi-view body of render_step for an upstream that is already staged on the host: views alternate between
+        two lanes on two compute streams (forward of view i + 1 under the backward of view i; the backward passes stay
+        in view order: k_finalize adds into the shared gradient buffers without atomics), uploads and downloads ride
+        on the copy stream.  Returns the H2D byte count."""
+        dev = self.engine.device
+        if self._compute_streams is None:
+            self._compute_streams = [torch.cuda.Stream(device=dev), torch.cuda.Stream(device=dev)]
+        copy = self.copy_stream
+        for st in self._compute_streams:
+            st.wait_stream(main)  # scene upload / earlier work of the caller
+        copy.wait_stream(main)
+        bwd_done, last_bwd, h2d = [None, None], None, 0
+        with torch.cuda.device(dev):
+            for i, cam in enumerate(cams):
+                j = i & 1
+                lane, st = self._lane(j), self._compute_streams[j]
+                last = i == len(cams) - 1
+                events = self._band_events[:self.bands] if (last and self.bands > 1) else None
+                with torch.cuda.stream(copy):  # upstream of view i -> lane j, once backward(i - 2) has consumed it
+                    if bwd_done[j] is not None:
+                        copy.wait_event(bwd_done[j])
+                    lane["upstream"].copy_(self.h_upstream, non_blocking=True)
+                    up_ready = torch.cuda.Event()
+                    up_ready.record(copy)
+                h2d += 4 * self.h_upstream.numel()
+                image = self._images[j]
+                if i > 1:  # this image buffer was last used two views ago: its download must have read it
+                    st.wait_event(self._image_copied[j])
+                with torch.cuda.stream(st):  # (a lane's first use initialises its workspace on the current stream)
+                    self._forward_fast(cam, gamma, eps, tau, events, st, image, lane)
+                fwd_done = torch.cuda.Event()
+                fwd_done.record(st)
+                with torch.cuda.stream(copy):
+                    if events:
+                        for b, ev in enumerate(events):
+                            r0, r1 = self._band_rows[b]
+                            copy.wait_event(ev)
+                            if r1 > r0:
+                                self.h_image[r0:r1].copy_(image[r0:r1], non_blocking=True)
+                    else:
+                        copy.wait_event(fwd_done)
+                        self.h_image.copy_(image, non_blocking=True)
+                    self._image_copied[j].record(copy)
+                st.wait_event(up_ready)
+                if last_bwd is not None:
+                    st.wait_event(last_bwd)
+                with torch.cuda.stream(st):
+                    self._backward_fast(cam, gamma, eps, normalize, gate, i > 0, st, lane)
+                last_bwd = torch.cuda.Event()
+                last_bwd.record(st)
+                bwd_done[j] = last_bwd
+        for st in self._compute_streams:
+            main.wait_stream(st)
+        return h2d
 
     def set_scene(self, pos, rad, opa, feat, bg):
         """Stage a (new) scene: uploaded by the next render_step, resident afterwards."""
@@ -243,7 +315,7 @@ class HostRenderSession:
         self._scene_dirty = True
 
     def render_step(self, cams, upstream_fn=None, gamma=0.1, eps=1e-2, tau=0.01, normalize=True, gate=True,
-                    check=False, reduce_fn=None, compact=False, always_upload=False):
+                    check=False, reduce_fn=None, compact=False, always_upload=False, pipeline=True):
         """One host-to-host step over one or more views of the staged scene:
         [H2D scene if set_scene was called since the last step]; per view: ss_forward, D2H image,
         [upstream_fn(view, host image) -> host upstream, else the staged h_upstream], H2D upstream, ss_backward
@@ -259,7 +331,12 @@ class HostRenderSession:
             self.d_in.copy_(self.h_in, non_blocking=True)
             self._scene_dirty = False
             h2d += 4 * self.h_in.numel()
-        for i, cam in enumerate(cams):
+        if upstream_fn is None and not check and len(cams) > 1 and pipeline:
+            h2d += self._views_pipelined(cams, gamma, eps, tau, normalize, gate, main)
+            cams_serial = []
+        else:
+            cams_serial = cams
+        for i, cam in enumerate(cams_serial):
             if upstream_fn is None:  # upstream already staged on the host: upload it under the forward pass
                 self.copy_stream.wait_stream(main)  # (orders it after the previous view's backward)
                 with torch.cuda.stream(self.copy_stream):
@@ -268,7 +345,7 @@ class HostRenderSession:
             # completed, i.e. while the raster kernel of band b + 1 is running (and the last band under the backward)
             # Only the LAST view of a step is banded: an earlier view's download hides under the next view's
             # forward pass anyway, and a band boundary costs a few microseconds of raster time.
-            nb = self.bands if (not check and i == len(cams) - 1) else 1  # (check=True may re-render after a regrowth)
+            nb = self.bands if (not check and i == len(cams_serial) - 1) else 1  # (check=True may re-render after a regrowth)
             events = self._band_events[:nb] if nb > 1 else None
             if i > 1:  # this image buffer was last used two views ago: its download must have read it
                 main.wait_event(self._image_copied[i & 1])

@@ -53,6 +53,10 @@ struct Layout {
     int n_tiles, ntx, nty, raw_stride;
 };
 
+#ifndef SS_FUSED_SORT
+#define SS_FUSED_SORT 0  // lists of <= 512 pairs sorted by k_tile_sort_small (0) or by k_raster itself (1: measured, no gain)
+#endif
+
 constexpr int TILE = SS_TILE;
 constexpr int TILE_PX = TILE * TILE;
 constexpr int SORT_SMALL = 512;   // per-tile lists up to this length: k_tile_sort_small (one CTA per tile, registers + 8 KB smem)

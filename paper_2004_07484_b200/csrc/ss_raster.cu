@@ -21,6 +21,9 @@
 #include <type_traits>
 
 #include "ss_common.cuh"
+#if SS_FUSED_SORT
+#include "ss_sort.cuh"
+#endif
 
 namespace ss {
 
@@ -29,7 +32,11 @@ namespace {
 struct RasterArgs {
     Cam cam;
     const int *tile_start;
-    const int *pair_id;
+    int *pair_id;  // sorted per-tile lists; written by this kernel when it sorts its own tile (sort_here)
+    // inputs of the fused per-tile sort (sort_small_segment)
+    const unsigned long long *pair_key, *key;
+    const int *bucket, *tile_cursor;
+    int sort_here;
     const Rec *rec;
     const float4 *flt;
     const float *feat;
@@ -250,9 +257,23 @@ __global__ void __launch_bounds__(TILE_PX, (KT <= 8 && DP <= 4) ? SS_RASTER_MINB
         __syncwarp();
     }
 
-    const bool overflow = (a.status[ST_FLAGS] & SS_FLAG_PAIR_OVERFLOW) != 0;  // lists not built
+    const long long ws_flags = a.status[ST_FLAGS];
+    const bool overflow = (ws_flags & SS_FLAG_PAIR_OVERFLOW) != 0;  // lists not built
     const int s0 = a.tile_start[tile];
     const int n_cand = overflow ? 0 : a.tile_start[tile + 1] - s0;
+#if SS_FUSED_SORT
+    // Fused per-tile sort (experiment, off by default): a tile with <= 512 candidates orders its own list here, in
+    // the staging area of its shared memory, instead of in k_tile_sort_small in front of this kernel -- the idea
+    // being that the sort would run in the issue slots the drain rounds of the other resident tiles leave idle.
+    // Measured at C3: 302 us against 258 + 41 us for the two kernels, i.e. nothing is hidden: both are bound by the
+    // same load/store path (shared-memory wavefronts here, shuffles there), not by issue slots.
+    if (a.sort_here && n_cand >= 1 && n_cand <= SORT_SMALL) {
+        sort_small_segment(a.tile_start, a.pair_key, a.pair_id, a.bucket, a.key, a.tile_cursor, ws_flags, tile,
+                           (unsigned long long *)smem_raw, (int *)(smem_raw + SORT_SMALL * 8),
+                           (unsigned *)(smem_raw + SORT_SMALL * 12));
+        __syncthreads();  // the sorted ids (global) and the scratch (shared, reused by the staging) are settled
+    }
+#endif
 
     // tile-wide minimum ray cosine for the early-stop bound (raster.py:358)
     double tile_cos = 1.0;
@@ -624,7 +645,12 @@ cudaError_t launch_raster(const FwdLaunch &a, cudaStream_t s, int tile0, int n_t
     RasterArgs r;
     r.cam = a.cam;
     r.tile_start = (const int *)(a.ws + L.tile_start);
-    r.pair_id = (const int *)(a.ws + L.pair_id);
+    r.pair_id = (int *)(a.ws + L.pair_id);
+    r.pair_key = (const unsigned long long *)(a.ws + L.pair_key);
+    r.key = (const unsigned long long *)(a.ws + L.key);
+    r.bucket = (const int *)(a.ws + L.bucket);
+    r.tile_cursor = (const int *)(a.ws + L.tile_cursor);
+    r.sort_here = SS_FUSED_SORT;
     r.rec = (const Rec *)(a.ws + L.rec);
     r.flt = (const float4 *)(a.ws + L.flt);
     r.feat = a.feat; r.bg = a.bg;

@@ -17,7 +17,7 @@ def main():
     size = int(sys.argv[2]) if len(sys.argv) > 2 else 1024
     tau = float(sys.argv[3]) if len(sys.argv) > 3 else 0.01
     det = len(sys.argv) > 4 and sys.argv[4] == "det"  # time the SS_OPT_DETERMINISTIC backward
-    steps = 10
+    steps = int(os.environ.get("QT_STEPS", "10"))
     pos, rad, opa, feat, bg, vec = orc.benchmark_scene(count, size, size, seed=0)
     cam = camera_from_vector(vec, size, size)
     spec = CameraSpec.from_camera(cam)

@@ -65,6 +65,7 @@ class ViewShardedRenderer:
         self.collectives_issued = 0  # collective launches so far (one per step on NCCL)
         self._twin = None  # second engine + the two side streams of the pipelined view loop
         self._streams = None
+        self._graph = None  # captured local step (graphed_step)
 
     def _pipeline(self):
         """Two engines (workspaces) on two side streams, or None when the engine is a stand-in (CPU tests)."""
@@ -112,7 +113,7 @@ class ViewShardedRenderer:
 
     def step(self, scene, cameras: Sequence, upstream_fn: Callable, grads: SphereGradBuffer, gamma=0.1,
              eps=1e-2, tau=0.01, top_k=5, normalize=True, gate=True, camera_grads=True, check=False,
-             overlap=False, pipeline=True):
+             overlap=False, pipeline=True, _local_only=False):
         """One multi-view step.  scene = (pos, rad, opa, feat, bg) device tensors; cameras = the
         CameraSpec of EVERY view (all ranks hold the list); upstream_fn(view, image) -> dL/dimage.
         Fills `grads` with the sum over ALL views (after the allreduce) and returns
@@ -173,8 +174,50 @@ class ViewShardedRenderer:
                                        accumulate=(i > 0))  # the first local view overwrites: no zero fill
             if camera_grads:
                 cam_out[v] = res["cam_grad"]
-        if self.world_size > 1:
+        if self.world_size > 1 and not _local_only:
             self._pending = self._allreduce(grads)
             if not overlap:
                 self.finish()
         return cam_out
+
+    def graphed_step(self, scene, cameras: Sequence, upstream_fn: Callable, grads: SphereGradBuffer, overlap=False,
+                     **params):
+        """`step` with the local work of the step -- every kernel of every local view, on both pipeline streams, plus
+        whatever `upstream_fn` enqueues -- captured ONCE into a CUDA graph and replayed afterwards.  The usual
+        training loop renders a fixed set of cameras while the optimiser updates the scene tensors in place: the
+        launch sequence never changes, and a replay removes the launch gaps between the ~10 kernels of a view
+        (C1: 0.17 -> 0.04 ms per frame, C2: 0.15 -> 0.11 ms, C3: 0.496 -> 0.473 ms, `scripts/graph_probe.py`).
+
+        The graph bakes in the tensors' addresses, the cameras and the blend parameters: it is re-captured when any
+        of those changes (scene tensors replaced rather than updated in place, another camera list, other
+        `params`).  `upstream_fn` must be capturable (device work on the current stream, no host synchronisation)
+        and must depend on its arguments only.  check=True is not available (no host read inside a graph): poll
+        `engine.read_status()` yourself.  The collective of a multi-GPU step stays outside the graph."""
+        if params.get("check"):
+            raise ValueError("graphed_step cannot read the status block back (check=True): use step()")
+        params = dict(params, check=False)
+        key = (tuple((t.data_ptr(), tuple(t.shape)) for t in scene), tuple(id(c) for c in cameras), id(upstream_fn),
+               grads.flat.data_ptr(), tuple(sorted(params.items())))
+        g = self._graph
+        if g is None or g["key"] != key:
+            self.finish()
+            dev = self.engine.device
+            side = torch.cuda.Stream(device=dev)
+            side.wait_stream(torch.cuda.current_stream(dev))
+            with torch.cuda.stream(side):  # warm-up outside the capture: workspaces, twin engine, function attributes
+                for _ in range(2):
+                    self.step(scene, cameras, upstream_fn, grads, _local_only=True, **params)
+            torch.cuda.current_stream(dev).wait_stream(side)
+            torch.cuda.synchronize(dev)
+            graph = torch.cuda.CUDAGraph()
+            with torch.cuda.graph(graph):
+                cam_out = self.step(scene, cameras, upstream_fn, grads, _local_only=True, **params)
+            g = self._graph = {"key": key, "graph": graph, "cam_out": cam_out,
+                               "keepalive": (scene, list(cameras), upstream_fn, grads)}
+        self.finish()  # a deferred reduction of the previous step must be done before the buffers are overwritten
+        g["graph"].replay()
+        if self.world_size > 1:
+            self._pending = self._allreduce(grads)
+            if not overlap:
+                self.finish()
+        return g["cam_out"]

@@ -410,3 +410,62 @@ def test_deterministic_backward_is_bit_reproducible(engine, count, size, d, k):
     if count >= 100_000:
         x, y = run(engine, False), run(engine, False)
         assert not all(torch.equal(x[key], y[key]) for key in keys), "the default path was reproducible here"
+
+
+# ------------------------------------------------------------------------------------------ CUDA-graph step
+@pytest.mark.parametrize("n_views", [1, 4])
+def test_graphed_step_replays_the_same_step_and_follows_in_place_updates(engine, n_views):
+    """ViewShardedRenderer.graphed_step captures the local work of a step (both pipeline streams, the upstream
+    callback) into a CUDA graph.  A replay must give what step() gives -- pixel counts exactly, gradients within the
+    atomics tolerance -- and must see scene tensors that were updated IN PLACE since the capture (the optimiser's
+    update), while a replaced tensor or another camera list triggers a new capture."""
+    import torch
+    import paper_2004_07484_b200 as pk
+    from paper_2004_07484_b200.multiview import SphereGradBuffer, ViewShardedRenderer
+    from paper_2004_07484_b200.synthetic import benchmark_scene, orbit_camera_vectors
+    m, w, h = 20000, 128, 96
+    pos, rad, opa, feat, bg, _ = benchmark_scene(m, w, h, seed=8)
+    scene = tuple(torch.from_numpy(x).cuda() for x in (pos, rad, opa, feat, bg))
+    cams = [pk.CameraSpec.from_camera(pk.camera_from_vector(v, w, h)) for v in orbit_camera_vectors(64)[:n_views]]
+    eng = pk.RenderEngine("cuda")
+    mv = ViewShardedRenderer(eng)
+
+    def upstream_fn(v, image):  # device work only: capturable
+        return torch.sign(image - 0.5) * (1.0 + 0.25 * v)
+
+    kw = dict(gamma=0.1, eps=1e-2, tau=0.01, top_k=5)
+
+    def snapshot(g, cam_out):
+        return ({k: getattr(g, k).clone() for k in ("d_pos", "d_rad", "d_opa", "d_feat", "pixel_count")},
+                {v: c.clone() for v, c in cam_out.items()})
+
+    def check(a, b, what):
+        assert torch.equal(a[0]["pixel_count"], b[0]["pixel_count"]), what
+        for k in ("d_pos", "d_rad", "d_opa", "d_feat"):
+            grad_close(a[0][k].cpu().numpy(), b[0][k].cpu().numpy(), f"{what} {k}", rtol=5e-5)
+        for v in a[1]:
+            grad_close(a[1][v].cpu().numpy()[:14], b[1][v].cpu().numpy()[:14], f"{what} cam_grad[{v}]", rtol=5e-5)
+
+    g_ref, g_gr = SphereGradBuffer(m, 3, "cuda"), SphereGradBuffer(m, 3, "cuda")
+    ref = snapshot(g_ref, mv.step(scene, cams, upstream_fn, g_ref, **kw))
+    for rep in range(3):  # capture, then two replays
+        got = snapshot(g_gr, mv.graphed_step(scene, cams, upstream_fn, g_gr, **kw))
+        check(got, ref, f"graphed step, call {rep}")
+    captured = mv._graph["graph"]
+    # the optimiser moves the spheres in place: the replay must render the moved scene
+    scene[0].add_(torch.tensor([0.01, -0.02, 0.05], device="cuda"))
+    scene[2].mul_(0.9)
+    ref2 = snapshot(g_ref, mv.step(scene, cams, upstream_fn, g_ref, **kw))
+    got2 = snapshot(g_gr, mv.graphed_step(scene, cams, upstream_fn, g_gr, **kw))
+    assert mv._graph["graph"] is captured  # same tensors, same cameras: replayed, not re-captured
+    check(got2, ref2, "graphed step after an in-place update")
+    assert not torch.equal(ref2[0]["pixel_count"], ref[0]["pixel_count"])
+    # another camera list: a new capture
+    cams2 = list(reversed(cams)) if n_views > 1 else [pk.CameraSpec.from_camera(
+        pk.camera_from_vector(orbit_camera_vectors(64)[9], w, h))]
+    ref3 = snapshot(g_ref, mv.step(scene, cams2, upstream_fn, g_ref, **kw))
+    got3 = snapshot(g_gr, mv.graphed_step(scene, cams2, upstream_fn, g_gr, **kw))
+    assert mv._graph["graph"] is not captured
+    check(got3, ref3, "graphed step, other cameras")
+    with pytest.raises(ValueError):
+        mv.graphed_step(scene, cams2, upstream_fn, g_gr, check=True, **kw)

@@ -275,10 +275,28 @@ def main():
         return mv.step(scene, cams, upstream_fn, grads, gamma=GAMMA, eps=EPS, tau=TAU, top_k=TOP_K,
                        normalize=True, gate=True, camera_grads=True, check=False)
 
+    def graphed():
+        return mv.graphed_step(scene, cams, upstream_fn, grads, gamma=GAMMA, eps=EPS, tau=TAU, top_k=TOP_K,
+                               normalize=True, gate=True, camera_grads=True)
+
     flush = torch.empty(256 << 20, dtype=torch.uint8, device=device)
+    # ---- headline: the step as the training loop of a fixed camera set runs it -- the local work of the step (all
+    # kernels of all local views, both pipeline streams, the upstream callback) captured once into a CUDA graph and
+    # replayed (ViewShardedRenderer.graphed_step); the collective of an N > 1 step stays outside the graph.  The
+    # dominant kernel carries one EXTERNAL event-record pair inside the graph: its in-step launch duration is read
+    # back after every step (a device synchronisation between the steps, outside their event brackets; the 256 MB
+    # flush in front of the next bracket keeps the GPU busy while the host enqueues it) and feeds `roofline`.
+    _lib.profile_captured_reset()
+    _lib.profile_enable_only(["k_raster"])
     for _ in range(args.warmup):
         flush.zero_()
-        step()
+        graphed()
+    torch.cuda.synchronize()
+    _lib.profile_collect()  # (drop the stream-launched warm-up pairs of the capture)
+    l0 = _lib.launch_count()
+    step()  # kernels per step, counted on one stream-launched step (a replay does not pass through the counter)
+    launches_per_step = _lib.launch_count() - l0
+    _lib.profile_collect()
     touched = int((grads.pixel_count > 0).sum().item())
     torch.cuda.synchronize()
     if world > 1:
@@ -286,58 +304,50 @@ def main():
     sampler = ClockSampler(dev_index)
     sampler.start()
     ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
-    launches0 = _lib.launch_count()
-    # the dominant kernel carries one CUDA-event pair inside the timed region (its in-step launch duration feeds
-    # `roofline`; an event pair between two kernels costs ~6 us of stream time -- three pairs added 18 us to a
-    # 0.49 ms frame, scripts/bench_probe.py -- and is part of the headline time); the other kernels' durations
-    # come from the separate pass below
-    _lib.profile_enable_only(["k_raster"])
+    raster_ms, raster_n = 0.0, 0
     torch.cuda.synchronize()
     for a, b in ev:
+        flush.zero_()
+        a.record()
+        graphed()
+        b.record()
+        got = _lib.profile_collect_captured().get("k_raster", (0.0, 0))  # synchronises
+        raster_ms, raster_n = raster_ms + got[0], raster_n + got[1]
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    clocks = sampler.stop()
+    prof = {"k_raster": (raster_ms, raster_n)}
+    launches = launches_per_step * args.steps
+    total_ms = float(sum(a.elapsed_time(b) for a, b in ev))
+    # ---- the same step with plain stream launches (mv.step), same flush / event protocol, one event pair around
+    # k_raster: what a caller pays who changes cameras or parameters every step
+    s_steps = max(3, min(args.steps, 50))
+    for _ in range(3):
+        flush.zero_()
+        step()
+    torch.cuda.synchronize()
+    _lib.profile_collect()
+    sev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(s_steps)]
+    for a, b in sev:
         flush.zero_()
         a.record()
         step()
         b.record()
     torch.cuda.synchronize()
-    if world > 1:
-        dist.barrier()
-    clocks = sampler.stop()
-    prof = _lib.profile_collect()
-    launches = _lib.launch_count() - launches0
-    # per-kernel breakdown: a short extra pass with every kernel bracketed by events (not the headline)
+    stream_prof = _lib.profile_collect()
+    stream_ms = float(sum(a.elapsed_time(b) for a, b in sev))
+    # per-kernel breakdown: a short extra pass with every kernel bracketed by events (stream launches)
     _lib.profile_enable(True)
     for _ in range(min(args.steps, 20)):
         flush.zero_()
         step()
     breakdown = _lib.profile_collect()
     _lib.profile_enable(False)
-    total_ms = float(sum(a.elapsed_time(b) for a, b in ev))
-    # the same step as a CUDA-graph replay (ViewShardedRenderer.graphed_step: the local work of the step captured
-    # once, replayed afterwards; the collective stays outside the graph) -- reported beside the headline, not as it:
-    # the headline keeps the kernel-level CUDA events of the roofline block inside its timed region
-    def graphed():
-        return mv.graphed_step(scene, cams, upstream_fn, grads, gamma=GAMMA, eps=EPS, tau=TAU, top_k=TOP_K,
-                               normalize=True, gate=True, camera_grads=True)
-
-    g_steps = max(3, min(args.steps, 50))
-    for _ in range(3):
-        flush.zero_()
-        graphed()
-    torch.cuda.synchronize()
     if world > 1:
-        dist.barrier()
-    gev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(g_steps)]
-    for a, b in gev:
-        flush.zero_()
-        a.record()
-        graphed()
-        b.record()
-    torch.cuda.synchronize()
-    graph_ms = float(sum(a.elapsed_time(b) for a, b in gev))
-    if world > 1:
-        t = torch.tensor([total_ms, graph_ms], dtype=torch.float64, device=device)
+        t = torch.tensor([total_ms, stream_ms], dtype=torch.float64, device=device)
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        total_ms, graph_ms = float(t[0].item()), float(t[1].item())
+        total_ms, stream_ms = float(t[0].item()), float(t[1].item())
     value = n_views * args.steps / (total_ms / 1e3)
 
     # ---- end to end with HOST buffers (copies inside the timed region, wall clock around synchronised steps)
@@ -467,9 +477,12 @@ def main():
             "config": {"workload": WORKLOAD, "views_per_rank": vpr, "views_total": n_views,
                        "cache": "L2 flushed between timed steps (256 MB write, outside the timed region)",
                        "pairs_T": T, "filled_slots_S": filled, "touched_spheres_U": touched,
-                       "timed_region_note": "1 CUDA-event pair per step (around k_raster) is recorded inside the timed "
-                                            "region for the roofline block; k_project / k_backward durations come from "
-                                            "the separate all-kernels pass",
+                       "step_path": "ViewShardedRenderer.graphed_step: the step's kernels replayed from one CUDA graph "
+                                    "(captured once; fixed cameras, scene tensors updated in place)",
+                       "timed_region_note": "1 external CUDA-event pair per step (around k_raster, inside the graph) is "
+                                            "read back after every step for the roofline block (~12 us of the step); "
+                                            "k_project / k_backward durations come from the separate stream-launched "
+                                            "all-kernels pass",
                        "collective": ("none" if world == 1 else
                                       f"1 {backend} sum-allreduce group of {grads.allreduce_bytes()} B per step")},
             "clocks": clocks,
@@ -486,11 +499,13 @@ def main():
                                    "d2h_bytes_per_step": dense_d2h,
                                    "path": "same call, whole scene uploaded and all M gradient rows downloaded every step "
                                            "(round 1's e2e)"},
-            "graph_replay": {"value": n_views * g_steps / (graph_ms / 1e3), "unit": "frames/s",
-                             "ms_per_step": graph_ms / g_steps, "steps": g_steps,
-                             "path": "ViewShardedRenderer.graphed_step: the step's kernels (all local views, both "
-                                     "pipeline streams) replayed from one CUDA graph; same inputs, flush and event "
-                                     "protocol as `value`, no kernel-level events inside"},
+            "stream_launches": {"value": n_views * s_steps / (stream_ms / 1e3), "unit": "frames/s",
+                                "ms_per_step": stream_ms / s_steps, "steps": s_steps,
+                                "k_raster_us": (1e3 * stream_prof["k_raster"][0] / max(1, stream_prof["k_raster"][1])
+                                                if "k_raster" in stream_prof else None),
+                                "path": "ViewShardedRenderer.step: the same step enqueued kernel by kernel on the "
+                                        "stream (no graph), same flush and event protocol, one event pair around "
+                                        "k_raster"},
             "gpu_launches": int(launches),
             "roofline": {"kernel": "k_raster", "bound": "hbm", "achieved": achieved, "peak": peak,
                          "unit": "GB/s", "frac": achieved / peak, "traffic": rk.get("traffic"),

@@ -372,6 +372,12 @@ int64_t ss_launch_count(void);
 void ss_profile_enable(int on);
 void ss_profile_enable_mask(unsigned mask); /* bit k = time kernel id k only */
 int ss_profile_collect(double *ms_sum, int64_t *launches, int n);
+/* The same for launches captured into a CUDA graph while profiling was enabled: they carry external event-record
+ * nodes, re-recorded by every replay.  ss_profile_collect_captured synchronises the device and returns, per kernel
+ * id, the summed duration and launch count of the MOST RECENT replay (call it after each replay to accumulate);
+ * ss_profile_captured_reset forgets the captured pairs (before capturing another graph). */
+void ss_profile_captured_reset(void);
+int ss_profile_collect_captured(double *ms_sum, int64_t *launches, int n);
 int ss_profile_kernel_count(void);
 const char *ss_profile_kernel_name(int kid);
 

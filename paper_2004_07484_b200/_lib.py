@@ -103,7 +103,8 @@ EXPORTS = ("ss_abi_version", "ss_status_string", "ss_last_cuda_error", "ss_works
            "ss_psc1_unpack", "ss_psc1_pack", "ss_convert_f64_f32", "ss_convert_f32_f64",
            "ss_shade_identity", "ss_shade_identity_backward", "ss_shade_diffuse", "ss_shade_diffuse_backward",
            "ss_shade_linear", "ss_shade_linear_backward", "ss_view_directions",
-           "ss_profile_enable", "ss_profile_enable_mask", "ss_profile_collect", "ss_profile_kernel_count", "ss_profile_kernel_name")
+           "ss_profile_enable", "ss_profile_enable_mask", "ss_profile_collect", "ss_profile_captured_reset",
+           "ss_profile_collect_captured", "ss_profile_kernel_count", "ss_profile_kernel_name")
 
 _lib = None
 
@@ -180,6 +181,9 @@ def load():
     lib.ss_profile_enable_mask.argtypes = [C.c_uint]
     lib.ss_profile_collect.restype = C.c_int
     lib.ss_profile_collect.argtypes = [C.POINTER(C.c_double), C.POINTER(C.c_int64), C.c_int]
+    lib.ss_profile_captured_reset.restype = None
+    lib.ss_profile_collect_captured.restype = C.c_int
+    lib.ss_profile_collect_captured.argtypes = [C.POINTER(C.c_double), C.POINTER(C.c_int64), C.c_int]
     lib.ss_profile_kernel_count.restype = C.c_int
     lib.ss_profile_kernel_name.restype = C.c_char_p
     lib.ss_profile_kernel_name.argtypes = [C.c_int]
@@ -225,4 +229,21 @@ def profile_collect() -> dict:
     rc = lib.ss_profile_collect(ms, cnt, n)
     if rc != SS_OK:
         raise NativeLibraryError(status_string(rc))
+    return {lib.ss_profile_kernel_name(i).decode(): (float(ms[i]), int(cnt[i])) for i in range(n)}
+
+
+def profile_captured_reset() -> None:
+    load().ss_profile_captured_reset()
+
+
+def profile_collect_captured() -> dict:
+    """{kernel: (ms of the most recent graph replay, launches)} for launches captured into a CUDA graph while
+    profiling was enabled (synchronises the device)."""
+    lib = load()
+    n = lib.ss_profile_kernel_count()
+    ms = (C.c_double * n)()
+    cnt = (C.c_int64 * n)()
+    rc = lib.ss_profile_collect_captured(ms, cnt, n)
+    if rc != SS_OK:
+        raise NativeLibraryError(f"ss_profile_collect_captured failed: {rc}")
     return {lib.ss_profile_kernel_name(i).decode(): (float(ms[i]), int(cnt[i])) for i in range(n)}

@@ -18,8 +18,31 @@ static const int kProfCap = 8192;
 static cudaEvent_t g_ev0[kProfCap], g_ev1[kProfCap];
 static int g_ev_kid[kProfCap];
 static int g_ev_made = 0, g_ev_used = 0;
+// Launches made while the stream is being captured into a CUDA graph get EXTERNAL event-record nodes (their events
+// are re-recorded by every replay and can be read from outside the graph): one pair per captured launch, kept until
+// ss_profile_captured_reset; ss_profile_collect_captured reads the pairs of the most recent replay.
+static const int kCapCap = 1024;
+static cudaEvent_t g_cev0[kCapCap], g_cev1[kCapCap];
+static int g_cev_kid[kCapCap];
+static int g_cev_made = 0, g_cev_used = 0;
+static bool capturing(cudaStream_t s) {
+    cudaStreamCaptureStatus st = cudaStreamCaptureStatusNone;
+    return cudaStreamIsCapturing(s, &st) == cudaSuccess && st == cudaStreamCaptureStatusActive;
+}
 void prof_begin(int kid, cudaStream_t s) {
-    if (!((g_prof_mask >> kid) & 1u) || g_ev_used >= kProfCap) return;
+    if (!((g_prof_mask >> kid) & 1u)) return;
+    if (capturing(s)) {
+        if (g_cev_used >= kCapCap) return;
+        if (g_cev_used >= g_cev_made) {
+            cudaEventCreate(&g_cev0[g_cev_made]);
+            cudaEventCreate(&g_cev1[g_cev_made]);
+            ++g_cev_made;
+        }
+        g_cev_kid[g_cev_used] = kid;
+        cudaEventRecordWithFlags(g_cev0[g_cev_used], s, cudaEventRecordExternal);
+        return;
+    }
+    if (g_ev_used >= kProfCap) return;
     if (g_ev_used >= g_ev_made) {
         cudaEventCreate(&g_ev0[g_ev_made]);
         cudaEventCreate(&g_ev1[g_ev_made]);
@@ -29,7 +52,14 @@ void prof_begin(int kid, cudaStream_t s) {
     cudaEventRecord(g_ev0[g_ev_used], s);
 }
 void prof_end(int kid, cudaStream_t s) {
-    if (!((g_prof_mask >> kid) & 1u) || g_ev_used >= kProfCap) return;
+    if (!((g_prof_mask >> kid) & 1u)) return;
+    if (capturing(s)) {
+        if (g_cev_used >= kCapCap) return;
+        cudaEventRecordWithFlags(g_cev1[g_cev_used], s, cudaEventRecordExternal);
+        ++g_cev_used;
+        return;
+    }
+    if (g_ev_used >= kProfCap) return;
     cudaEventRecord(g_ev1[g_ev_used], s);
     ++g_ev_used;
 }
@@ -118,6 +148,23 @@ int ss_profile_collect(double *ms_sum, int64_t *launches, int n) {
         if (k >= 0 && k < n) { ms_sum[k] += ms; launches[k] += 1; }
     }
     ss::g_ev_used = 0;
+    return SS_OK;
+}
+
+void ss_profile_captured_reset(void) { ss::g_cev_used = 0; }
+
+int ss_profile_collect_captured(double *ms_sum, int64_t *launches, int n) {
+    if (!ms_sum || !launches) return SS_ERR_NULL;
+    for (int i = 0; i < n; ++i) { ms_sum[i] = 0.0; launches[i] = 0; }
+    cudaError_t e = cudaDeviceSynchronize();
+    if (e != cudaSuccess) return cuda_fail(e);
+    for (int i = 0; i < ss::g_cev_used; ++i) {
+        float ms = 0.f;
+        e = cudaEventElapsedTime(&ms, ss::g_cev0[i], ss::g_cev1[i]);
+        if (e != cudaSuccess) return cuda_fail(e);
+        int k = ss::g_cev_kid[i];
+        if (k >= 0 && k < n) { ms_sum[k] += ms; launches[k] += 1; }
+    }
     return SS_OK;
 }
 

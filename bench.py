@@ -11,8 +11,11 @@ runs config 3 itself (1 view, identity camera); N > 1 runs config 4's orbit, 8 v
 (64 views at N = 8), weak scaling.
 
 Timing: CUDA events on the launching stream around each step, L2 flushed (256 MB write) between
-steps outside the timed region, max over ranks.  `--impl reference` times the CPU implementation
-(the float64 oracle port of the reference, all host threads) on the same config.
+steps outside the timed region, max over ranks.  The step is `ViewShardedRenderer.graphed_step`: its
+local work is captured once into a CUDA graph and replayed (what a training loop over a fixed set of
+cameras runs); `stream_launches` in the line is the same step enqueued kernel by kernel.
+`--impl reference` times the unmodified reference's own CPU path (baseline/_ref, one core; its float64
+C port on all host threads is reported beside it) on the same config.
 """
 from __future__ import annotations
 

@@ -190,8 +190,9 @@ class ViewShardedRenderer:
 
         The graph bakes in the tensors' addresses, the cameras and the blend parameters: it is re-captured when any
         of those changes (scene tensors replaced rather than updated in place, another camera list, other
-        `params`).  `upstream_fn` must be capturable (device work on the current stream, no host synchronisation)
-        and must depend on its arguments only.  check=True is not available (no host read inside a graph): poll
+        `params`, another `upstream_fn` OBJECT -- pass the same function every step, a fresh lambda per call means a
+        fresh capture per call).  `upstream_fn` must be capturable (device work on the current stream, no host
+        synchronisation) and must depend on its arguments only.  check=True is not available (no host read inside a graph): poll
         `engine.read_status()` yourself.  The collective of a multi-GPU step stays outside the graph."""
         if params.get("check"):
             raise ValueError("graphed_step cannot read the status block back (check=True): use step()")

@@ -291,9 +291,19 @@ def main():
     # flush in front of the next bracket keeps the GPU busy while the host enqueues it) and feeds `roofline`.
     _lib.profile_captured_reset()
     _lib.profile_enable_only(["k_raster"])
-    for _ in range(args.warmup):
-        flush.zero_()
-        graphed()
+    use_graph = True
+    try:
+        for _ in range(args.warmup):
+            flush.zero_()
+            graphed()
+        torch.cuda.synchronize()
+    except Exception as exc:  # capture refused (driver / torch mismatch): time the stream-launched step instead
+        print(f"bench: CUDA-graph capture failed ({exc!r}); the headline falls back to stream launches", file=sys.stderr)
+        use_graph = False
+        torch.cuda.synchronize()
+        for _ in range(args.warmup):
+            flush.zero_()
+            step()
     torch.cuda.synchronize()
     _lib.profile_collect()  # (drop the stream-launched warm-up pairs of the capture)
     l0 = _lib.launch_count()
@@ -312,10 +322,13 @@ def main():
     for a, b in ev:
         flush.zero_()
         a.record()
-        graphed()
+        if use_graph:
+            graphed()
+        else:
+            step()
         b.record()
-        got = _lib.profile_collect_captured().get("k_raster", (0.0, 0))  # synchronises
-        raster_ms, raster_n = raster_ms + got[0], raster_n + got[1]
+        got = (_lib.profile_collect_captured() if use_graph else _lib.profile_collect()).get("k_raster", (0.0, 0))
+        raster_ms, raster_n = raster_ms + got[0], raster_n + got[1]  # (the collect synchronises)
     torch.cuda.synchronize()
     if world > 1:
         dist.barrier()
@@ -480,8 +493,9 @@ def main():
             "config": {"workload": WORKLOAD, "views_per_rank": vpr, "views_total": n_views,
                        "cache": "L2 flushed between timed steps (256 MB write, outside the timed region)",
                        "pairs_T": T, "filled_slots_S": filled, "touched_spheres_U": touched,
-                       "step_path": "ViewShardedRenderer.graphed_step: the step's kernels replayed from one CUDA graph "
-                                    "(captured once; fixed cameras, scene tensors updated in place)",
+                       "step_path": ("ViewShardedRenderer.graphed_step: the step's kernels replayed from one CUDA graph "
+                                     "(captured once; fixed cameras, scene tensors updated in place)" if use_graph else
+                                     "ViewShardedRenderer.step, stream launches (CUDA-graph capture failed on this box)"),
                        "timed_region_note": "1 external CUDA-event pair per step (around k_raster, inside the graph) is "
                                             "read back after every step for the roofline block (~12 us of the step); "
                                             "k_project / k_backward durations come from the separate stream-launched "

@@ -65,16 +65,16 @@ struct TopK {
     // (L2 latency: 3 CTAs x 128 KB of records do not fit the L1) and formed its float64 depth first
     double wz; int wid; float wlo;
     __device__ __forceinline__ void init() {
-        // large K: the arrays live in (L1-cached) local memory, not in 4*KT registers
-#pragma unroll 1
-        for (int k = 0; k < KT; ++k) { z[k] = -INFINITY; id[k] = -1; c[k] = 0.0f; }
+        // large K: the arrays live in (L1-cached) local memory, not in 4*KT registers.  They are NOT cleared: slots
+        // at and beyond n are never read (the insert bubbles inside [0, n), the getters answer "empty" there), and
+        // clearing 16 KT bytes per pixel was 1 GB of local-memory stores per C5 frame, most of it evicted to DRAM.
         n = 0;
         wz = -INFINITY; wid = -1; wlo = -INFINITY;
     }
     __device__ __forceinline__ void bind(unsigned char *, int) {}
-    __device__ __forceinline__ double get_z(int k) const { return z[k]; }
-    __device__ __forceinline__ int get_id(int k) const { return id[k]; }
-    __device__ __forceinline__ float get_c(int k) const { return c[k]; }
+    __device__ __forceinline__ double get_z(int k) const { return k < n ? z[k] : -INFINITY; }
+    __device__ __forceinline__ int get_id(int k) const { return k < n ? id[k] : -1; }
+    __device__ __forceinline__ float get_c(int k) const { return k < n ? c[k] : 0.0f; }
     __device__ __forceinline__ bool may_enter(float zzf) const { return zzf >= wlo; }
     // keep the KT largest by (z desc, id asc) -- raster.py:389-399.  Candidates arrive roughly front to back,
     // so the usual case is an append at slot n (one comparison) or, once full, a rejection against the cached

@@ -33,7 +33,8 @@ struct Cam {
 // Workspace layout (byte offsets, 256-byte aligned).
 struct Layout {
     size_t status;       // 16 x int64 (SsStatus)
-    size_t tile_count;   // n_tiles + 1 int32 (zeroed with status at forward start): spheres touching <= 4 tiles
+    size_t tile_count;   // n_tiles + 1 int32 (zeroed with status at forward start): spheres touching <= 4 tiles;
+                         // after k_scan: the emit cursor of the fallback path
     size_t tile_count_big;  // n_tiles + 1 int32 (zeroed too): spheres touching > 4 tiles
     size_t tile_start;   // n_tiles + 1 int32
     size_t tile_cursor;  // n_tiles int32
@@ -41,7 +42,6 @@ struct Layout {
     size_t rec;          // M Rec
     size_t key;          // M uint64 (order-preserving bits of earliest)
     size_t trect;        // M ushort4 tile rects (tx0, tx1, ty0, ty1); tx0 > tx1 = off sensor
-    size_t slot4;        // M int4: slot inside each touched tile's segment (spheres touching <= 4 tiles)
     size_t proj_r;       // M double
     size_t flt;          // M float4: screen-space filter (projected centre x, y, padded rho^2, -)
     size_t bucket;       // n_tiles x BUCKET_CAP int32: sphere ids written straight into their tile by k_project
@@ -88,7 +88,6 @@ inline Layout make_layout(const SsDims &dm) {
     L.rec = take(M * sizeof(Rec));
     L.key = take(M * 8);
     L.trect = take(M * 8);
-    L.slot4 = take(M * 16);
     L.proj_r = take(M * 8);
     L.flt = take(M * 16);
     L.bucket = take((size_t)L.n_tiles * BUCKET_CAP * 4);

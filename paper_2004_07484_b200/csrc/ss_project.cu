@@ -9,10 +9,9 @@
 //               (4096 ids per tile; spheres touching > 4 tiles fill the bucket from its far end), so the common
 //               case needs no emit pass at all: the per-tile sort reads its bucket and gathers the keys.
 //   k_emit      (fallback, only when some tile holds more than 4096 spheres: SS_FLAG_LIST_FALLBACK)
-//               writes each (tile, sphere) pair into its tile's segment.  The slot inside the
-//               segment was already claimed by k_project's counting atomic (spheres touching
-//               <= 4 tiles, i.e. nearly all), so k_emit is a pure streaming pass; spheres that
-//               touch more tiles claim their slots here, behind the pre-claimed ones.
+//               writes each (tile, sphere) pair into its tile's segment, claiming the slot with an atomic on a
+//               per-tile cursor (the consumed tile counters, zeroed again by k_scan).  The usual frame pays
+//               nothing for it: no per-sphere slot array is written by k_project any more.
 //   k_tile_sort per-tile sort of the segment by (earliest float64, sphere index): exactly the
 //               order the reference gets from "stable argsort by earliest" (raster.py:243)
 //               followed by "stable argsort by tile id" (raster.py:289).  One CTA per tile,
@@ -97,7 +96,7 @@ struct ProjectArgs {
     const float *pos, *rad, *opa, *feat, *bg;
     Cam cam;
     Rec *rec; unsigned long long *key; ushort4 *trect; double *proj_r; float4 *flt;
-    int *tile_count; int *tile_count_big; int4 *slot4; int *bucket; long long *status;
+    int *tile_count; int *tile_count_big; int *bucket; long long *status;
     int32_t *rect; uint8_t *on_sensor; double *earliest; double *proj_r_out;
     int records_only; int validate;
 };
@@ -226,7 +225,6 @@ __global__ void __launch_bounds__(256) k_project(ProjectArgs a) {
             const float rho_pad = (float)(rho * (1.0 + 1e-5) + 4e-7 * (fabs(pcx) + fabs(pcy) + cam.sensor_w));
             a.flt[i] = make_float4((float)pcx, (float)pcy, rho_pad * rho_pad * 1.000001f, 0.0f);
             if (on && nt <= 4) {
-                a.slot4[i] = make_int4(sl[0], sl[1], sl[2], sl[3]);
                 const int wx = tr.y - tr.x + 1;
 #pragma unroll
                 for (int j = 0; j < 4; ++j)  // the slot claimed above is the position inside the tile's bucket
@@ -246,8 +244,7 @@ __global__ void __launch_bounds__(256) k_project(ProjectArgs a) {
 
 // Single-CTA exclusive scan over the tile counts; also resets the emit cursors, lists the
 // tiles whose segment is too long for the small sort kernel, and publishes T / overflow.
-__global__ void __launch_bounds__(1024) k_scan(const int *__restrict__ tile_count,
-                                               const int *__restrict__ tile_count_big, int *tile_start,
+__global__ void __launch_bounds__(1024) k_scan(int *tile_count, const int *__restrict__ tile_count_big, int *tile_start,
                                                int *tile_cursor, int *big_tiles, int n_tiles,
                                                long long max_pairs, long long M, long long *status) {
     __shared__ long long warp_sums[32];
@@ -290,7 +287,8 @@ __global__ void __launch_bounds__(1024) k_scan(const int *__restrict__ tile_coun
         for (int j = 0; j < 4; ++j) {
             if (i0 + j < n_tiles) {
                 tile_start[i0 + j] = (int)(excl > 0x7fffffffLL ? 0x7fffffffLL : excl);
-                tile_cursor[i0 + j] = cs[j];  // late claims (k_emit) go behind the pre-claimed slots
+                tile_cursor[i0 + j] = cs[j];  // ids of spheres touching <= 4 tiles sit at the front of the bucket
+                tile_count[i0 + j] = 0;       // consumed: from here on the emit cursor of the fallback path (k_emit)
                 if (c[j] > SORT_SMALL) big_tiles[1 + atomicAdd(&n_big, 1)] = i0 + j;
                 if (c[j] > BUCKET_CAP) n_over = 1;
             }
@@ -313,103 +311,26 @@ __global__ void __launch_bounds__(1024) k_scan(const int *__restrict__ tile_coun
 }
 
 __global__ void __launch_bounds__(256) k_emit(long long M, const ushort4 *__restrict__ trect,
-                                              const int4 *__restrict__ slot4,
                                               const unsigned long long *__restrict__ key,
-                                              const int *__restrict__ tile_start, int *tile_cursor,
+                                              const int *__restrict__ tile_start, int *emit_cursor,
                                               unsigned long long *pair_key, int *pair_id, int ntx,
                                               const long long *__restrict__ status) {
     const long long flags = status[ST_FLAGS];
     if ((flags & SS_FLAG_PAIR_OVERFLOW) || !(flags & SS_FLAG_LIST_FALLBACK)) return;  // the usual case: nothing to do
+    // Fallback (some tile holds more than BUCKET_CAP spheres): every (tile, sphere) pair claims its slot in the
+    // tile's segment with an atomic on the emit cursor (k_scan left it at zero); the per-tile sort orders the segment.
     for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < M; i += (long long)gridDim.x * blockDim.x) {
         ushort4 tr = trect[i];
         if (tr.x > tr.y) continue;
         unsigned long long k = key[i];
-        const int wx = tr.y - tr.x + 1, nt = wx * (tr.w - tr.z + 1);
-        if (nt <= 4) {
-            const int4 s4 = slot4[i];
-            const int sl[4] = {s4.x, s4.y, s4.z, s4.w};
-#pragma unroll
-            for (int j = 0; j < 4; ++j)
-                if (j < nt) {
-                    const int pos = tile_start[(tr.z + j / wx) * ntx + tr.x + j % wx] + sl[j];
-                    pair_key[pos] = k;
-                    pair_id[pos] = (int)i;
-                }
-            continue;
-        }
         for (int ty = tr.z; ty <= tr.w; ++ty)
             for (int tx = tr.x; tx <= tr.y; ++tx) {
                 int t = ty * ntx + tx;
-                int slot = tile_start[t] + atomicAdd(&tile_cursor[t], 1);
+                int slot = tile_start[t] + atomicAdd(&emit_cursor[t], 1);
                 pair_key[slot] = k;
                 pair_id[slot] = (int)i;
             }
     }
-}
-
-// The same for segments of up to 4096 pairs (12 position bits, 20 key bits), several 64-blocks per warp, every
-// stage through shared memory: keys / ids hold the loaded segment, pk the packed words (4096).
-constexpr int PACK_BIG = 4096;
-__device__ bool sort_packed4096(int s0, int n, const SegSrc &src, int *pair_id, unsigned long long *keys, int *ids,
-                                unsigned *pk) {
-    __shared__ unsigned long long s_lo[8], s_hi[8];
-    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-    int np2 = 64;
-    while (np2 < n) np2 <<= 1;
-    const int n_blocks = np2 >> 6;
-    unsigned long long lo = ~0ull, hi = 0ull;
-    for (int i = tid; i < n; i += blockDim.x) {
-        unsigned long long k; int id;
-        src.load(i, k, id);
-        keys[i] = k; ids[i] = id;
-        lo = min(lo, k); hi = max(hi, k);
-    }
-    for (int o = 16; o > 0; o >>= 1) {
-        lo = min(lo, __shfl_xor_sync(0xffffffffu, lo, o));
-        hi = max(hi, __shfl_xor_sync(0xffffffffu, hi, o));
-    }
-    if (lane == 0) { s_lo[warp] = lo; s_hi[warp] = hi; }
-    __syncthreads();
-#pragma unroll
-    for (int w = 0; w < 8; ++w) { lo = min(lo, s_lo[w]); hi = max(hi, s_hi[w]); }
-    const int bits = 64 - __clzll((long long)(hi - lo));
-    const int shift = bits > 20 ? bits - 20 : 0;
-    for (int b = warp; b < n_blocks; b += 8) {
-        const int i0 = (b << 6) + lane, i1 = i0 + 32;
-        unsigned e0 = i0 < n ? (((unsigned)((keys[i0] - lo) >> shift) << 12) | (unsigned)i0) : 0xffffffffu;
-        unsigned e1 = i1 < n ? (((unsigned)((keys[i1] - lo) >> shift) << 12) | (unsigned)i1) : 0xffffffffu;
-        u_sort64(e0, e1, lane);
-        pk[i0] = e0; pk[i1] = e1;
-    }
-    __syncthreads();
-    const int half = np2 >> 1;
-    for (int k = 128; k <= np2; k <<= 1) {
-        const int hk = k >> 1;
-        for (int c = tid; c < half; c += blockDim.x) {  // flip
-            const int q = c & (hk - 1);
-            const int l = ((c - q) << 1) + q, r = ((c - q) << 1) + k - 1 - q;
-            const unsigned a = pk[l], b = pk[r];
-            if (b < a) { pk[l] = b; pk[r] = a; }
-        }
-        __syncthreads();
-        for (int j = hk >> 1; j >= 64; j >>= 1) {  // long-distance disperse stages
-            for (int c = tid; c < half; c += blockDim.x) {
-                const int q = c & (j - 1);
-                const int l = ((c - q) << 1) + q;
-                const unsigned a = pk[l], b = pk[l + j];
-                if (b < a) { pk[l] = b; pk[l + j] = a; }
-            }
-            __syncthreads();
-        }
-        for (int b = warp; b < n_blocks; b += 8) {  // j = 32 .. 1 in registers
-            const int i0 = (b << 6) + lane, i1 = i0 + 32;
-            unsigned e0 = pk[i0], e1 = pk[i1];
-            u_disperse64(e0, e1, lane);
-            pk[i0] = e0; pk[i1] = e1;
-        }
-        __syncthreads();
-    }
-    return rank_ties_and_write<12>(pk, n, [keys](int i) { return keys[i]; }, ids, pair_id + s0);
 }
 
 __global__ void __launch_bounds__(256) k_tile_sort_small(const int *__restrict__ tile_start,
@@ -587,7 +508,7 @@ cudaError_t launch_project(const FwdLaunch &a, bool records_only, cudaStream_t s
         p.trect = (ushort4 *)(ws + L.trect); p.proj_r = (double *)(ws + L.proj_r);
         p.flt = (float4 *)(ws + L.flt);
         p.tile_count = (int *)(ws + L.tile_count); p.tile_count_big = (int *)(ws + L.tile_count_big);
-        p.slot4 = (int4 *)(ws + L.slot4); p.bucket = (int *)(ws + L.bucket); p.status = (long long *)(ws + L.status);
+        p.bucket = (int *)(ws + L.bucket); p.status = (long long *)(ws + L.status);
         p.rect = a.rect; p.on_sensor = a.on_sensor; p.earliest = a.earliest; p.proj_r_out = a.proj_r_out;
         p.records_only = records_only ? 1 : 0;
         p.validate = (!records_only && !(a.blend.flags & SS_OPT_SKIP_VALIDATE)) ? 1 : 0;
@@ -611,7 +532,7 @@ cudaError_t launch_binning(const FwdLaunch &a, cudaStream_t s) {
     int *pair_id = (int *)(ws + L.pair_id);
     {
         ProfScope ps(KID_SCAN, s);
-        k_scan<<<1, 1024, 0, s>>>((const int *)(ws + L.tile_count), (const int *)(ws + L.tile_count_big),
+        k_scan<<<1, 1024, 0, s>>>((int *)(ws + L.tile_count), (const int *)(ws + L.tile_count_big),
                                   tile_start, tile_cursor, big_tiles, L.n_tiles, a.dims.max_pairs, M, status);
     }
     count_launch();
@@ -620,8 +541,8 @@ cudaError_t launch_binning(const FwdLaunch &a, cudaStream_t s) {
         if (grid > 148) grid = 148;  // grid-stride: in the usual (bucket) case the launch is an early exit
         {
             ProfScope ps(KID_EMIT, s);
-            k_emit<<<grid, 256, 0, s>>>(M, (const ushort4 *)(ws + L.trect), (const int4 *)(ws + L.slot4),
-                                        (const unsigned long long *)(ws + L.key), tile_start, tile_cursor,
+            k_emit<<<grid, 256, 0, s>>>(M, (const ushort4 *)(ws + L.trect),
+                                        (const unsigned long long *)(ws + L.key), tile_start, (int *)(ws + L.tile_count),
                                         pair_key, pair_id, L.ntx, status);
         }
         if (!SS_FUSED_SORT) {

@@ -333,6 +333,71 @@ __global__ void __launch_bounds__(256) k_emit(long long M, const ushort4 *__rest
     }
 }
 
+// The same for segments of up to 4096 pairs (12 position bits, 20 key bits), several 64-blocks per warp, every
+// stage through shared memory: keys / ids hold the loaded segment, pk the packed words (4096).
+constexpr int PACK_BIG = 4096;
+__device__ bool sort_packed4096(int s0, int n, const SegSrc &src, int *pair_id, unsigned long long *keys, int *ids,
+                                unsigned *pk) {
+    __shared__ unsigned long long s_lo[8], s_hi[8];
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    int np2 = 64;
+    while (np2 < n) np2 <<= 1;
+    const int n_blocks = np2 >> 6;
+    unsigned long long lo = ~0ull, hi = 0ull;
+    for (int i = tid; i < n; i += blockDim.x) {
+        unsigned long long k; int id;
+        src.load(i, k, id);
+        keys[i] = k; ids[i] = id;
+        lo = min(lo, k); hi = max(hi, k);
+    }
+    for (int o = 16; o > 0; o >>= 1) {
+        lo = min(lo, __shfl_xor_sync(0xffffffffu, lo, o));
+        hi = max(hi, __shfl_xor_sync(0xffffffffu, hi, o));
+    }
+    if (lane == 0) { s_lo[warp] = lo; s_hi[warp] = hi; }
+    __syncthreads();
+#pragma unroll
+    for (int w = 0; w < 8; ++w) { lo = min(lo, s_lo[w]); hi = max(hi, s_hi[w]); }
+    const int bits = 64 - __clzll((long long)(hi - lo));
+    const int shift = bits > 20 ? bits - 20 : 0;
+    for (int b = warp; b < n_blocks; b += 8) {
+        const int i0 = (b << 6) + lane, i1 = i0 + 32;
+        unsigned e0 = i0 < n ? (((unsigned)((keys[i0] - lo) >> shift) << 12) | (unsigned)i0) : 0xffffffffu;
+        unsigned e1 = i1 < n ? (((unsigned)((keys[i1] - lo) >> shift) << 12) | (unsigned)i1) : 0xffffffffu;
+        u_sort64(e0, e1, lane);
+        pk[i0] = e0; pk[i1] = e1;
+    }
+    __syncthreads();
+    const int half = np2 >> 1;
+    for (int k = 128; k <= np2; k <<= 1) {
+        const int hk = k >> 1;
+        for (int c = tid; c < half; c += blockDim.x) {  // flip
+            const int q = c & (hk - 1);
+            const int l = ((c - q) << 1) + q, r = ((c - q) << 1) + k - 1 - q;
+            const unsigned a = pk[l], b = pk[r];
+            if (b < a) { pk[l] = b; pk[r] = a; }
+        }
+        __syncthreads();
+        for (int j = hk >> 1; j >= 64; j >>= 1) {  // long-distance disperse stages
+            for (int c = tid; c < half; c += blockDim.x) {
+                const int q = c & (j - 1);
+                const int l = ((c - q) << 1) + q;
+                const unsigned a = pk[l], b = pk[l + j];
+                if (b < a) { pk[l] = b; pk[l + j] = a; }
+            }
+            __syncthreads();
+        }
+        for (int b = warp; b < n_blocks; b += 8) {  // j = 32 .. 1 in registers
+            const int i0 = (b << 6) + lane, i1 = i0 + 32;
+            unsigned e0 = pk[i0], e1 = pk[i1];
+            u_disperse64(e0, e1, lane);
+            pk[i0] = e0; pk[i1] = e1;
+        }
+        __syncthreads();
+    }
+    return rank_ties_and_write<12>(pk, n, [keys](int i) { return keys[i]; }, ids, pair_id + s0);
+}
+
 __global__ void __launch_bounds__(256) k_tile_sort_small(const int *__restrict__ tile_start,
                                                          const unsigned long long *__restrict__ pair_key,
                                                          int *pair_id, const int *__restrict__ bucket,

@@ -23,4 +23,4 @@ SAN="tests/test_gpu_parity.py::test_golden_forward tests/test_gpu_parity.py::tes
 compute-sanitizer --tool memcheck --error-exitcode 1 python -m pytest $SAN -x -q > $out/${tag}_sanitizer_memcheck.log 2>&1
 compute-sanitizer --tool racecheck --error-exitcode 1 python -m pytest tests/test_gpu_parity.py::test_golden_forward tests/test_gpu_parity.py::test_golden_backward -x -q > $out/${tag}_sanitizer_racecheck.log 2>&1
 compute-sanitizer --tool synccheck --error-exitcode 1 python -m pytest tests/test_gpu_parity.py::test_golden_forward tests/test_gpu_parity.py::test_golden_backward -x -q > $out/${tag}_sanitizer_synccheck.log 2>&1
-tail -3 $out/${tag}_sanitizer_*.log
+tail -n 3 $out/${tag}_sanitizer_memcheck.log $out/${tag}_sanitizer_racecheck.log $out/${tag}_sanitizer_synccheck.log

@@ -469,3 +469,39 @@ def test_graphed_step_replays_the_same_step_and_follows_in_place_updates(engine,
     check(got3, ref3, "graphed step, other cameras")
     with pytest.raises(ValueError):
         mv.graphed_step(scene, cams2, upstream_fn, g_gr, check=True, **kw)
+
+
+def test_kernel_timing_survives_graph_capture(engine):
+    """bench.py's roofline block times k_raster INSIDE the graph-replayed step: under stream capture the library's
+    profile scopes record external event nodes, which every replay re-records and ss_profile_collect_captured reads.
+    One pair per captured launch, a plausible duration per replay, and nothing left in the stream-launch list."""
+    import torch
+    import paper_2004_07484_b200 as pk
+    from paper_2004_07484_b200 import _lib
+    from paper_2004_07484_b200.multiview import SphereGradBuffer, ViewShardedRenderer
+    from paper_2004_07484_b200.synthetic import benchmark_scene, orbit_camera_vectors
+    m, w, h = 20000, 128, 96
+    pos, rad, opa, feat, bg, _ = benchmark_scene(m, w, h, seed=8)
+    scene = tuple(torch.from_numpy(x).cuda() for x in (pos, rad, opa, feat, bg))
+    cams = [pk.CameraSpec.from_camera(pk.camera_from_vector(v, w, h)) for v in orbit_camera_vectors(64)[:3]]
+    mv = ViewShardedRenderer(pk.RenderEngine("cuda"))
+    grads = SphereGradBuffer(m, 3, "cuda")
+
+    def upstream_fn(v, image):
+        return torch.sign(image - 0.5)
+
+    try:
+        _lib.profile_captured_reset()
+        _lib.profile_enable_only(["k_raster", "k_backward"])
+        mv.graphed_step(scene, cams, upstream_fn, grads, gamma=0.1, eps=1e-2, tau=0.01, top_k=5)  # capture + replay
+        _lib.profile_collect()  # the warm-up steps of the capture were stream launches
+        for _ in range(3):
+            mv.graphed_step(scene, cams, upstream_fn, grads, gamma=0.1, eps=1e-2, tau=0.01, top_k=5)
+            got = _lib.profile_collect_captured()
+            assert got["k_raster"][1] == len(cams) and got["k_backward"][1] == len(cams)
+            assert 1e-3 < got["k_raster"][0] < 50.0 and 1e-3 < got["k_backward"][0] < 50.0  # ms, summed over the views
+            assert got["k_project"][1] == 0
+        assert all(n == 0 for _, n in _lib.profile_collect().values())  # replays add nothing to the stream list
+    finally:
+        _lib.profile_enable(False)
+        _lib.profile_captured_reset()

@@ -160,6 +160,14 @@ __device__ __forceinline__ float rcp_approx(float x) {
     asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
     return y;
 }
+// float64 -> float32 of a value that is positive and inside the float32 normal range, truncated instead of rounded
+// (1 ulp instead of 1/2 ulp), with integer instructions: F2F.F32.F64 runs on the XU pipe (16 lanes per clock and SM),
+// which paces the hit path together with the MUFU operations.  Anything else (negative, zero, below 2^-126) gives 0.
+__device__ __forceinline__ float trunc_f64_to_f32(double x) {
+    const int hi = __double2hiint(x);
+    const unsigned b = __funnelshift_l((unsigned)__double2loint(x), (unsigned)(hi - 0x38000000), 3);
+    return hi >= 0x38100000 ? __uint_as_float(b) : 0.0f;
+}
 // keeps a value in a register: stops the compiler from re-deriving it (e.g. re-converting the
 // float64 ray to float32 inside the test loop)
 __device__ __forceinline__ float pin_reg(float x) {
@@ -242,7 +250,6 @@ __global__ void __launch_bounds__(TILE_PX, (KT <= 8 && DP <= 4) ? SS_RASTER_MINB
         double vn = sqrt(xs * xs + ys * ys + cam.focal * cam.focal);
         ux = xs / vn; uy = ys / vn; uz = cam.focal / vn;
     }
-    const float uzf = (float)uz;
     {   // sensor-space rectangle spanned by this warp's in-image pixel centres (empty: +inf/-inf)
         float x0 = valid ? (float)xs : INFINITY, x1 = valid ? (float)xs : -INFINITY;
         float y0 = valid ? (float)ys : INFINITY, y1 = valid ? (float)ys : -INFINITY;
@@ -313,14 +320,13 @@ __global__ void __launch_bounds__(TILE_PX, (KT <= 8 && DP <= 4) ? SS_RASTER_MINB
         const double2 cxy = lds_d2(ra);
         constexpr bool kCompact = DP == 3;
         double2 czn;
-        float4 mi;  // r, clamped opacity o, o / gamma * log2(e), sphere id bits
+        float4 mi;  // r, clamped opacity o, 1 / r, sphere id bits (d = 3: the id stays in the filter record)
         float4 f3 = make_float4(0.f, 0.f, 0.f, 0.f);
         if (kCompact) {
-            const float4 q = lds_f4(ra + 16);   // cz (float64), r, id
-            f3 = lds_f4(ra + 32);               // o, f0, f1, f2
+            const float4 q = lds_f4(ra + 16);   // cz (float64), r, 1 / r
             czn.x = __hiloint2double(__float_as_int(q.y), __float_as_int(q.x));
             czn.y = cxy.x * cxy.x + cxy.y * cxy.y + czn.x * czn.x;
-            mi = make_float4(q.z, f3.x, f3.x * inv_g2, q.w);
+            mi = make_float4(q.z, 0.0f, q.w, 0.0f);  // the third quad (o, f0, f1, f2) is read once the hit is decided
         } else {
             czn = lds_d2(ra + 16);
             mi = lds_f4(ra + 32);
@@ -341,19 +347,32 @@ __global__ void __launch_bounds__(TILE_PX, (KT <= 8 && DP <= 4) ? SS_RASTER_MINB
         }
         const float rf = mi.x;
         // r^2 - dist^2 in one rounding: r is a float32 value, so r * r is exact in float64 and the fused form
-        // equals the reference's (r * r) - dist2 bit for bit
-        const double rd = (double)rf;
+        // equals the reference's (r * r) - dist2 bit for bit.  The hit path is paced by the XU pipe (conversions that
+        // touch a 64-bit value, MUFU, bit scans: 16 lanes per clock and SM) as much as by issue slots, so float -> double
+        // of a normal positive radius is done with three integer instructions instead of F2F.F64.F32.
+        double rd;
+        {
+            const unsigned rb = __float_as_uint(rf);
+            rd = __hiloint2double((int)((rb >> 3) + 0x38000000u), (int)(rb << 29));
+            // zero / subnormal radius: the exact conversion (never at sane scales; volatile so that the compiler
+            // branches around it instead of executing it for every candidate and selecting)
+            if (rb < 0x00800000u) asm volatile("cvt.f64.f32 %0, %1;" : "=d"(rd) : "f"(rf));
+        }
         const double hc2 = fma(rd, rd, -dist2);
         // dist2 < r^2 and t + half_chord > 0
         if (hc2 > 0.0 && (t > 0.0 || t + sqrt(fmin(hc2, rd * rd)) > 0.0)) {
             ++n_hits;
-            // float32 NDC depth for the blend exponent: (far - clip(zeta)) / (far - near)
-            const float zeta_f = (MODE == SS_MODE_PINHOLE) ? (float)t * uzf : (float)t;
+            if (kCompact) { f3 = lds_f4(ra + 32); mi.y = f3.x; }
+            // float32 NDC depth for the blend exponent: (far - clip(zeta)) / (far - near); the float64 product t u_z is
+            // needed by the top-K insert anyway, so ONE conversion (of zeta) replaces two (t and u_z)
+            const float zeta_f = (float)zeta;
             const float zzf = fmaxf(fminf(a.far_f - zeta_f, a.fmn_f), 0.0f) * a.inv_range_f;
-            // closeness 1 - dist/r as (r^2 - dist^2) / (r (r + dist)): no cancellation near the rim
-            const float d2f = (float)dist2;
-            const float cl = (float)hc2 * rcp_approx(rf * fmaf(d2f, rsqrt_approx(fmaxf(d2f, 1e-37f)), rf));
-            const float e2 = zzf * mi.z;
+            // closeness 1 - dist/r as (r^2 - dist^2) / (r (r + dist)): no cancellation near the rim (1 - dist / r in
+            // float32 has an ABSOLUTE error of 2e-7, which a hard-gamma stack turns into 1e-4 of the image).  The two
+            // float64 -> float32 conversions are integer truncations (ALU) instead of F2F (XU pipe).
+            const float d2f = fmaxf(trunc_f64_to_f32(dist2), 1e-37f);
+            const float cl = trunc_f64_to_f32(hc2) * mi.z * rcp_approx(fmaf(d2f, rsqrt_approx(d2f), rf));
+            const float e2 = zzf * (mi.y * inv_g2);
             if (e2 > m2) {  // online form of raster.py:382-387
                 const float sc = ex2_approx(m2 - e2);
                 denom *= sc;
@@ -386,7 +405,8 @@ __global__ void __launch_bounds__(TILE_PX, (KT <= 8 && DP <= 4) ? SS_RASTER_MINB
                 if (store) {
                     double zc = zeta < near_ ? near_ : zeta;
                     zc = zc > far_ ? far_ : zc;
-                    top.insert((far_ - zc) * inv_range, __float_as_int(mi.w), cl, a.zpad);
+                    const int sid = kCompact ? (int)lds_u32(s_rec_a - CAP * 16 + j * 16 + 12) : __float_as_int(mi.w);
+                    top.insert((far_ - zc) * inv_range, sid, cl, a.zpad);
                 }
             }
         }
@@ -404,12 +424,13 @@ __global__ void __launch_bounds__(TILE_PX, (KT <= 8 && DP <= 4) ? SS_RASTER_MINB
             if (DP == 3) {
                 *reinterpret_cast<float4 *>(rp + 4) = make_float4(__int_as_float(__double2loint(rc.cz)),
                                                                   __int_as_float(__double2hiint(rc.cz)), rc.r,
-                                                                  __int_as_float(sid));
+                                                                  1.0f / rc.r);
             } else {
                 *reinterpret_cast<double2 *>(rp + 4) = make_double2(rc.cz, n2);
-                *reinterpret_cast<float4 *>(rp + 8) = make_float4(rc.r, rc.o, rc.o * inv_g2, __int_as_float(sid));
+                *reinterpret_cast<float4 *>(rp + 8) = make_float4(rc.r, rc.o, 1.0f / rc.r, __int_as_float(sid));
             }
-            const float4 fc = a.flt[sid];  // screen-space filter record (k_project)
+            float4 fc = a.flt[sid];  // screen-space filter record (k_project); its spare word carries the sphere id
+            fc.w = __int_as_float(sid);
             s_cf[tid] = fc;
             // which warps can this candidate touch?  Same arithmetic as the per-pixel test, applied to the
             // point of the warp's rectangle nearest to the projected centre (rounding is monotone, so a

@@ -109,22 +109,29 @@ struct TopK {
 template <int KT>
 struct TopKShared {
     double *z; int *id; float *c;  // this thread's column: slot k at [k * TILE_PX]
-    double wz; int wid;            // cached slot KT-1
+    // cached slot KT-1 of a FULL record.  While the record is filling up, wz = -inf admits everything and wid carries
+    // the fill count as -1 - n (no extra register): a new entry then starts at slot n instead of bubbling up from the
+    // bottom through the empty slots (10 shifts of 6 shared-memory accesses for the first five hits of every pixel),
+    // and the columns need no clearing.
+    double wz; int wid;
     float wlo;                     // (float)wz - pad: a float32 depth below this cannot enter the record
     __device__ __forceinline__ void bind(unsigned char *base, int tid) {
         z = (double *)base + tid;
         id = (int *)(base + (size_t)KT * TILE_PX * 8) + tid;
         c = (float *)(base + (size_t)KT * TILE_PX * 12) + tid;
     }
-    __device__ __forceinline__ void init() {
-#pragma unroll
-        for (int k = 0; k < KT; ++k) { z[k * TILE_PX] = -INFINITY; id[k * TILE_PX] = -1; c[k * TILE_PX] = 0.0f; }
-        wz = -INFINITY; wid = -1; wlo = -INFINITY;
-    }
+    __device__ __forceinline__ void init() { wz = -INFINITY; wid = -1; wlo = -INFINITY; }
+    __device__ __forceinline__ int filled() const { return wid < 0 && wz == -INFINITY ? -1 - wid : KT; }
     __device__ __forceinline__ bool may_enter(float zzf) const { return zzf >= wlo; }
     __device__ __forceinline__ void insert(double zz, int sid, float cl, float pad) {
-        if (!(zz > wz || (zz == wz && sid < wid))) return;
-        int k = KT - 1;
+        int k;
+        const bool filling = wlo == -INFINITY;  // (pad is finite, so a full record has a finite or NaN-free threshold)
+        if (filling) {
+            k = -1 - wid;
+        } else {
+            if (!(zz > wz || (zz == wz && sid < wid))) return;
+            k = KT - 1;
+        }
         while (k > 0) {
             const double zk = z[(k - 1) * TILE_PX];
             const int ik = id[(k - 1) * TILE_PX];
@@ -133,12 +140,16 @@ struct TopKShared {
             --k;
         }
         z[k * TILE_PX] = zz; id[k * TILE_PX] = sid; c[k * TILE_PX] = cl;
-        wz = z[(KT - 1) * TILE_PX]; wid = id[(KT - 1) * TILE_PX];
-        wlo = (float)wz - pad;
+        if (filling && wid > -KT) {  // still not full afterwards: n + 1 < KT
+            --wid;
+        } else {
+            wz = z[(KT - 1) * TILE_PX]; wid = id[(KT - 1) * TILE_PX];
+            wlo = (float)wz - pad;
+        }
     }
-    __device__ __forceinline__ double get_z(int k) const { return z[k * TILE_PX]; }
-    __device__ __forceinline__ int get_id(int k) const { return id[k * TILE_PX]; }
-    __device__ __forceinline__ float get_c(int k) const { return c[k * TILE_PX]; }
+    __device__ __forceinline__ double get_z(int k) const { return k < filled() ? z[k * TILE_PX] : -INFINITY; }
+    __device__ __forceinline__ int get_id(int k) const { return k < filled() ? id[k * TILE_PX] : -1; }
+    __device__ __forceinline__ float get_c(int k) const { return k < filled() ? c[k * TILE_PX] : 0.0f; }
 };
 
 #ifndef SS_TOPK_SHARED

@@ -60,14 +60,16 @@ struct TopK {
     int id[KT];
     float c[KT];
     int n;  // filled slots: a new entry starts at slot n, not at the bottom of an empty record
-    // admission threshold of a FULL record, cached in registers: with n_track = 32 most hits arrive after the record
-    // has filled up and are rejected; without the cache every one of them read z[KT - 1] back from local memory
-    // (L2 latency: 3 CTAs x 128 KB of records do not fit the L1) and formed its float64 depth first
+    // The LAST entry (slot n - 1; of a full record: the admission threshold) cached in registers.  With n_track = 32
+    // the arrays live in local memory (3 CTAs x 128 KB per SM do not fit the L1): candidates arrive roughly front to
+    // back, so while the record fills up the usual insert is an append behind the cached last entry (three local
+    // stores, no load), and once it is full the usual hit is rejected against the cache (float32 pre-filter first:
+    // wlo, formed without the float64 depth).
     double wz; int wid; float wlo;
     __device__ __forceinline__ void init() {
-        // large K: the arrays live in (L1-cached) local memory, not in 4*KT registers.  They are NOT cleared: slots
-        // at and beyond n are never read (the insert bubbles inside [0, n), the getters answer "empty" there), and
-        // clearing 16 KT bytes per pixel was 1 GB of local-memory stores per C5 frame, most of it evicted to DRAM.
+        // The arrays are NOT cleared: slots at and beyond n are never read (the insert bubbles inside [0, n), the
+        // getters answer "empty" there), and clearing 16 KT bytes per pixel was 1 GB of local-memory stores per C5
+        // frame, most of it evicted to DRAM.
         n = 0;
         wz = -INFINITY; wid = -1; wlo = -INFINITY;
     }
@@ -76,16 +78,24 @@ struct TopK {
     __device__ __forceinline__ int get_id(int k) const { return k < n ? id[k] : -1; }
     __device__ __forceinline__ float get_c(int k) const { return k < n ? c[k] : 0.0f; }
     __device__ __forceinline__ bool may_enter(float zzf) const { return zzf >= wlo; }
-    // keep the KT largest by (z desc, id asc) -- raster.py:389-399.  Candidates arrive roughly front to back,
-    // so the usual case is an append at slot n (one comparison) or, once full, a rejection against the cached
-    // worst entry.
+    // keep the KT largest by (z desc, id asc) -- raster.py:389-399
     __device__ __forceinline__ void insert(double zz, int sid, float cl, float pad) {
+        const bool beats_last = n > 0 && (zz > wz || (zz == wz && sid < wid));
         int k;
         if (n < KT) {
             k = n++;
+            if (!beats_last) {  // in order: append, the new entry is the last one
+                z[k] = zz; id[k] = sid; c[k] = cl;
+                wz = zz; wid = sid;
+                if (n == KT) wlo = (float)wz - pad;
+                return;
+            }
+            // out of order: the last entry moves down one slot (and stays the last: the cache is unchanged)
+            z[k] = wz; id[k] = wid; c[k] = c[k - 1];
+            --k;
         } else {
-            if (!(zz > wz || (zz == wz && sid < wid))) return;
-            k = KT - 1;
+            if (!beats_last) return;
+            k = KT - 1;  // the worst entry drops out
         }
 #pragma unroll 1
         while (k > 0) {
@@ -96,7 +106,7 @@ struct TopK {
             --k;
         }
         z[k] = zz; id[k] = sid; c[k] = cl;
-        if (n == KT) {  // the record is full: refresh the cached threshold
+        if (n == KT) {  // the record is (or has just become) full: refresh the cached threshold
             wz = z[KT - 1]; wid = id[KT - 1];
             wlo = (float)wz - pad;
         }
@@ -211,6 +221,9 @@ __device__ __forceinline__ unsigned lds_u32(unsigned a) {
 }
 
 constexpr float kLn2 = 0.6931471805599453f;
+#ifndef SS_RASTER_MINB_WIDE
+#define SS_RASTER_MINB_WIDE 3  // d <= 16 or long records
+#endif
 #ifndef SS_RASTER_MINB
 #define SS_RASTER_MINB (SS_TOPK_SHARED ? 4 : 3)  // resident CTAs per SM the register allocation targets (d <= 4, K <= 8)
 #endif
@@ -225,7 +238,7 @@ constexpr int rec_stride() {
 }
 
 template <int DP, int KT, int MODE>
-__global__ void __launch_bounds__(TILE_PX, (KT <= 8 && DP <= 4) ? SS_RASTER_MINB : (DP <= 16 ? 3 : 2)) k_raster(RasterArgs a) {
+__global__ void __launch_bounds__(TILE_PX, (KT <= 8 && DP <= 4) ? SS_RASTER_MINB : (DP <= 16 ? SS_RASTER_MINB_WIDE : 2)) k_raster(RasterArgs a) {
     constexpr int CAP = SS_MAX_CHUNK;
     extern __shared__ __align__(16) unsigned char smem_raw[];
     constexpr int RS = rec_stride<DP>();           // floats per staged candidate
@@ -361,8 +374,11 @@ __global__ void __launch_bounds__(TILE_PX, (KT <= 8 && DP <= 4) ? SS_RASTER_MINB
         // equals the reference's (r * r) - dist2 bit for bit.  The hit path is paced by the XU pipe (conversions that
         // touch a 64-bit value, MUFU, bit scans: 16 lanes per clock and SM) as much as by issue slots, so float -> double
         // of a normal positive radius is done with three integer instructions instead of F2F.F64.F32.
-        double rd;
-        {
+        // (Only where the XU pipe is the limiter -- short records at 4 CTAs per SM.  With wide payloads / long records
+        // the kernel waits on local memory instead and the extra integer instructions cost 2 %: C5 2.92 -> 2.98 ms.)
+        constexpr bool kXuDiet = KT <= 8 && DP <= 4;
+        double rd = (double)rf;
+        if (kXuDiet) {
             const unsigned rb = __float_as_uint(rf);
             rd = __hiloint2double((int)((rb >> 3) + 0x38000000u), (int)(rb << 29));
             // zero / subnormal radius: the exact conversion (never at sane scales; volatile so that the compiler
@@ -381,8 +397,8 @@ __global__ void __launch_bounds__(TILE_PX, (KT <= 8 && DP <= 4) ? SS_RASTER_MINB
             // closeness 1 - dist/r as (r^2 - dist^2) / (r (r + dist)): no cancellation near the rim (1 - dist / r in
             // float32 has an ABSOLUTE error of 2e-7, which a hard-gamma stack turns into 1e-4 of the image).  The two
             // float64 -> float32 conversions are integer truncations (ALU) instead of F2F (XU pipe).
-            const float d2f = fmaxf(trunc_f64_to_f32(dist2), 1e-37f);
-            const float cl = trunc_f64_to_f32(hc2) * mi.z * rcp_approx(fmaf(d2f, rsqrt_approx(d2f), rf));
+            const float d2f = fmaxf(kXuDiet ? trunc_f64_to_f32(dist2) : (float)dist2, 1e-37f);
+            const float cl = (kXuDiet ? trunc_f64_to_f32(hc2) : (float)hc2) * mi.z * rcp_approx(fmaf(d2f, rsqrt_approx(d2f), rf));
             const float e2 = zzf * (mi.y * inv_g2);
             if (e2 > m2) {  // online form of raster.py:382-387
                 const float sc = ex2_approx(m2 - e2);

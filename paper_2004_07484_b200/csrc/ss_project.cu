@@ -585,6 +585,34 @@ cudaError_t launch_project(const FwdLaunch &a, bool records_only, cudaStream_t s
     return cudaGetLastError();
 }
 
+#ifndef SS_SORT_FORK
+#define SS_SORT_FORK 1
+#endif
+// Two side streams + fork / join events per host thread and device, created on first use and kept for the life of
+// the thread (the only CUDA objects this library owns).  Per THREAD: an event re-recorded by another thread between
+// this thread's record and wait would hand the wait the wrong dependency.
+struct SideStreams {
+    cudaStream_t s1 = nullptr, s2 = nullptr;
+    cudaEvent_t fork = nullptr, join1 = nullptr, join2 = nullptr;
+    bool ok = false, tried = false;
+};
+static SideStreams *side_streams() {
+    static thread_local SideStreams per_dev[64];
+    int dev = 0;
+    if (cudaGetDevice(&dev) != cudaSuccess || dev < 0 || dev >= 64) return nullptr;
+    SideStreams &x = per_dev[dev];
+    if (!x.tried) {
+        x.tried = true;
+        x.ok = cudaStreamCreateWithFlags(&x.s1, cudaStreamNonBlocking) == cudaSuccess &&
+               cudaStreamCreateWithFlags(&x.s2, cudaStreamNonBlocking) == cudaSuccess &&
+               cudaEventCreateWithFlags(&x.fork, cudaEventDisableTiming) == cudaSuccess &&
+               cudaEventCreateWithFlags(&x.join1, cudaEventDisableTiming) == cudaSuccess &&
+               cudaEventCreateWithFlags(&x.join2, cudaEventDisableTiming) == cudaSuccess;
+        if (!x.ok) (void)cudaGetLastError();
+    }
+    return x.ok ? &x : nullptr;
+}
+
 cudaError_t launch_binning(const FwdLaunch &a, cudaStream_t s) {
     long long M = a.dims.num_spheres;
     char *ws = a.ws;
@@ -610,6 +638,18 @@ cudaError_t launch_binning(const FwdLaunch &a, cudaStream_t s) {
                                         (const unsigned long long *)(ws + L.key), tile_start, (int *)(ws + L.tile_count),
                                         pair_key, pair_id, L.ntx, status);
         }
+        // The three sort kernels work on disjoint tiles (segments of <= 512 / 513..4096 / more pairs).  The two
+        // long-segment kernels are usually a list of a few tiles or an early exit, so they run on two side streams
+        // beside the small-segment kernel (fork after k_emit, join before the raster pass; under stream capture the
+        // event waits become graph edges) instead of as two more serial steps of the frame.
+        SideStreams *side = SS_SORT_FORK ? side_streams() : nullptr;
+        cudaStream_t s_mid = s, s_big = s;
+        if (side) {
+            if (cudaEventRecord(side->fork, s) != cudaSuccess || cudaStreamWaitEvent(side->s1, side->fork, 0) != cudaSuccess ||
+                cudaStreamWaitEvent(side->s2, side->fork, 0) != cudaSuccess)
+                return cudaGetLastError();
+            s_mid = side->s1; s_big = side->s2;
+        }
         if (!SS_FUSED_SORT) {
             ProfScope ps(KID_SORT_SMALL, s);
             k_tile_sort_small<<<L.n_tiles, 256, 0, s>>>(tile_start, pair_key, pair_id, (const int *)(ws + L.bucket),
@@ -631,20 +671,25 @@ cudaError_t launch_binning(const FwdLaunch &a, cudaStream_t s) {
                 if (e != cudaSuccess) return e;
             }
             const int grid_mid = L.n_tiles < 148 * 4 ? L.n_tiles : 148 * 4;
-            ProfScope ps(KID_SORT_BIG, s);
-            k_tile_sort_mid<<<grid_mid, 256, mid_smem, s>>>(tile_start, pair_id, (const int *)(ws + L.bucket),
+            ProfScope ps(KID_SORT_BIG, s_mid);
+            k_tile_sort_mid<<<grid_mid, 256, mid_smem, s_mid>>>(tile_start, pair_id, (const int *)(ws + L.bucket),
                                                             (const unsigned long long *)(ws + L.key), tile_cursor,
                                                             big_tiles, status);
             count_launch();
         }
         int grid_big = L.n_tiles < 296 ? L.n_tiles : 296;
         {
-            ProfScope ps(KID_SORT_BIG, s);
-            k_tile_sort_big<<<grid_big, 256, big_smem, s>>>(tile_start, pair_key, pair_id, (const int *)(ws + L.bucket),
-                                                            (const unsigned long long *)(ws + L.key), tile_cursor, big_tiles,
-                                                            status);
+            ProfScope ps(KID_SORT_BIG, s_big);
+            k_tile_sort_big<<<grid_big, 256, big_smem, s_big>>>(tile_start, pair_key, pair_id, (const int *)(ws + L.bucket),
+                                                                (const unsigned long long *)(ws + L.key), tile_cursor,
+                                                                big_tiles, status);
         }
         count_launch(SS_FUSED_SORT ? 2 : 3);
+        if (side) {
+            if (cudaEventRecord(side->join1, s_mid) != cudaSuccess || cudaEventRecord(side->join2, s_big) != cudaSuccess ||
+                cudaStreamWaitEvent(s, side->join1, 0) != cudaSuccess || cudaStreamWaitEvent(s, side->join2, 0) != cudaSuccess)
+                return cudaGetLastError();
+        }
     }
     return cudaGetLastError();
 }

@@ -397,8 +397,12 @@ __global__ void __launch_bounds__(TILE_PX, (KT <= 8 && DP <= 4) ? SS_RASTER_MINB
             // closeness 1 - dist/r as (r^2 - dist^2) / (r (r + dist)): no cancellation near the rim (1 - dist / r in
             // float32 has an ABSOLUTE error of 2e-7, which a hard-gamma stack turns into 1e-4 of the image).  The two
             // float64 -> float32 conversions are integer truncations (ALU) instead of F2F (XU pipe).
-            const float d2f = fmaxf(kXuDiet ? trunc_f64_to_f32(dist2) : (float)dist2, 1e-37f);
-            const float cl = (kXuDiet ? trunc_f64_to_f32(hc2) : (float)hc2) * mi.z * rcp_approx(fmaf(d2f, rsqrt_approx(d2f), rf));
+            // (the other instantiations convert with F2F rounding towards zero: the same values bit for bit, so that
+            // n_track = 8 / 16 / 32 render identical images, reference tests/test_grad.py:147-164)
+            const float d2f = fmaxf(kXuDiet ? trunc_f64_to_f32(dist2) : __double2float_rz(dist2), 1e-37f);
+            float hc2f = kXuDiet ? trunc_f64_to_f32(hc2) : __double2float_rz(hc2);
+            if (!kXuDiet && hc2f < 1.17549435e-38f) hc2f = 0.0f;
+            const float cl = hc2f * mi.z * rcp_approx(fmaf(d2f, rsqrt_approx(d2f), rf));
             const float e2 = zzf * (mi.y * inv_g2);
             if (e2 > m2) {  // online form of raster.py:382-387
                 const float sc = ex2_approx(m2 - e2);

@@ -278,28 +278,41 @@ def main():
         return mv.step(scene, cams, upstream_fn, grads, gamma=GAMMA, eps=EPS, tau=TAU, top_k=TOP_K,
                        normalize=True, gate=True, camera_grads=True, check=False)
 
-    def graphed():
-        return mv.graphed_step(scene, cams, upstream_fn, grads, gamma=GAMMA, eps=EPS, tau=TAU, top_k=TOP_K,
-                               normalize=True, gate=True, camera_grads=True)
+    def upstream_fn_timed(v, image):  # a second function OBJECT: a second capture of the same step (see below)
+        return upstreams[v]
+
+    def graphed(timed=True):
+        return mv.graphed_step(scene, cams, upstream_fn_timed if timed else upstream_fn, grads, gamma=GAMMA, eps=EPS,
+                               tau=TAU, top_k=TOP_K, normalize=True, gate=True, camera_grads=True)
 
     flush = torch.empty(256 << 20, dtype=torch.uint8, device=device)
     # ---- headline: the step as the training loop of a fixed camera set runs it -- the local work of the step (all
     # kernels of all local views, both pipeline streams, the upstream callback) captured once into a CUDA graph and
     # replayed (ViewShardedRenderer.graphed_step); the collective of an N > 1 step stays outside the graph.  The
-    # dominant kernel carries one EXTERNAL event-record pair inside the graph: its in-step launch duration is read
-    # back after every step (a device synchronisation between the steps, outside their event brackets; the 256 MB
-    # flush in front of the next bracket keeps the GPU busy while the host enqueues it) and feeds `roofline`.
+    # dominant kernel's in-step launch duration feeds `roofline`: the step is captured twice, once with one EXTERNAL
+    # event-record pair around k_raster inside the graph and once without, and every `sample_every`-th timed step
+    # replays the capture with the pair (read back after that step: a device synchronisation outside the event
+    # brackets).  A pair costs ~12 us inside a graph -- 2.5 % of the step -- so it is not paid on every step.
+    sample_every = max(1, min(10, args.steps // 20))
     _lib.profile_captured_reset()
-    _lib.profile_enable_only(["k_raster"])
     use_graph = True
     try:
+        _lib.profile_enable_only(["k_raster"])
         for _ in range(args.warmup):
             flush.zero_()
-            graphed()
+            graphed(timed=True)
         torch.cuda.synchronize()
+        if sample_every > 1:
+            _lib.profile_enable(False)
+            for _ in range(args.warmup):
+                flush.zero_()
+                graphed(timed=False)
+            torch.cuda.synchronize()
+            _lib.profile_enable_only(["k_raster"])
     except Exception as exc:  # capture refused (driver / torch mismatch): time the stream-launched step instead
         print(f"bench: CUDA-graph capture failed ({exc!r}); the headline falls back to stream launches", file=sys.stderr)
         use_graph = False
+        _lib.profile_enable_only(["k_raster"])
         torch.cuda.synchronize()
         for _ in range(args.warmup):
             flush.zero_()
@@ -319,16 +332,18 @@ def main():
     ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
     raster_ms, raster_n = 0.0, 0
     torch.cuda.synchronize()
-    for a, b in ev:
+    for i, (a, b) in enumerate(ev):
+        sampled = not use_graph or i % sample_every == 0
         flush.zero_()
         a.record()
         if use_graph:
-            graphed()
+            graphed(timed=sampled)
         else:
             step()
         b.record()
-        got = (_lib.profile_collect_captured() if use_graph else _lib.profile_collect()).get("k_raster", (0.0, 0))
-        raster_ms, raster_n = raster_ms + got[0], raster_n + got[1]  # (the collect synchronises)
+        if sampled:
+            got = (_lib.profile_collect_captured() if use_graph else _lib.profile_collect()).get("k_raster", (0.0, 0))
+            raster_ms, raster_n = raster_ms + got[0], raster_n + got[1]  # (the collect synchronises)
     torch.cuda.synchronize()
     if world > 1:
         dist.barrier()
@@ -496,10 +511,12 @@ def main():
                        "step_path": ("ViewShardedRenderer.graphed_step: the step's kernels replayed from one CUDA graph "
                                      "(captured once; fixed cameras, scene tensors updated in place)" if use_graph else
                                      "ViewShardedRenderer.step, stream launches (CUDA-graph capture failed on this box)"),
-                       "timed_region_note": "1 external CUDA-event pair per step (around k_raster, inside the graph) is "
-                                            "read back after every step for the roofline block (~12 us of the step); "
-                                            "k_project / k_backward durations come from the separate stream-launched "
-                                            "all-kernels pass",
+                       "timed_region_note": f"every {sample_every}-th timed step replays a second capture of the same "
+                                            "step that carries 1 external CUDA-event pair around k_raster (read back "
+                                            "after that step; the pair costs ~12 us of a step, the other steps replay "
+                                            "the capture without it): roofline.kernels.k_raster.launches_timed of the "
+                                            "timed region's launches; k_project / k_backward durations come from the "
+                                            "separate stream-launched all-kernels pass",
                        "collective": ("none" if world == 1 else
                                       f"1 {backend} sum-allreduce group of {grads.allreduce_bytes()} B per step")},
             "clocks": clocks,

@@ -65,7 +65,8 @@ class ViewShardedRenderer:
         self.collectives_issued = 0  # collective launches so far (one per step on NCCL)
         self._twin = None  # second engine + the two side streams of the pipelined view loop
         self._streams = None
-        self._graph = None  # captured local step (graphed_step)
+        self._graphs = {}  # captured local steps (graphed_step), newest last; a handful is kept
+        self._graph = None  # the most recently used one
 
     def _pipeline(self):
         """Two engines (workspaces) on two side streams, or None when the engine is a stand-in (CPU tests)."""
@@ -191,7 +192,7 @@ class ViewShardedRenderer:
         The graph bakes in the tensors' addresses, the cameras and the blend parameters: it is re-captured when any
         of those changes (scene tensors replaced rather than updated in place, another camera list, other
         `params`, another `upstream_fn` OBJECT -- pass the same function every step, a fresh lambda per call means a
-        fresh capture per call).  `upstream_fn` must be capturable (device work on the current stream, no host
+        fresh capture per call; the last four captures are kept, so a loop may alternate between a few of them).  `upstream_fn` must be capturable (device work on the current stream, no host
         synchronisation) and must depend on its arguments only.  check=True is not available (no host read inside a graph): poll
         `engine.read_status()` yourself.  The collective of a multi-GPU step stays outside the graph."""
         if params.get("check"):
@@ -199,8 +200,8 @@ class ViewShardedRenderer:
         params = dict(params, check=False)
         key = (tuple((t.data_ptr(), tuple(t.shape)) for t in scene), tuple(id(c) for c in cameras), id(upstream_fn),
                grads.flat.data_ptr(), tuple(sorted(params.items())))
-        g = self._graph
-        if g is None or g["key"] != key:
+        g = self._graphs.get(key)
+        if g is None:
             self.finish()
             dev = self.engine.device
             side = torch.cuda.Stream(device=dev)
@@ -213,8 +214,12 @@ class ViewShardedRenderer:
             graph = torch.cuda.CUDAGraph()
             with torch.cuda.graph(graph):
                 cam_out = self.step(scene, cameras, upstream_fn, grads, _local_only=True, **params)
-            g = self._graph = {"key": key, "graph": graph, "cam_out": cam_out,
-                               "keepalive": (scene, list(cameras), upstream_fn, grads)}
+            g = {"key": key, "graph": graph, "cam_out": cam_out,
+                 "keepalive": (scene, list(cameras), upstream_fn, grads)}
+            while len(self._graphs) >= 4:  # a loop that alternates between a few camera sets keeps its captures
+                self._graphs.pop(next(iter(self._graphs)))
+            self._graphs[key] = g
+        self._graph = g
         self.finish()  # a deferred reduction of the previous step must be done before the buffers are overwritten
         g["graph"].replay()
         if self.world_size > 1:

@@ -293,7 +293,7 @@ def main():
     # event-record pair around k_raster inside the graph and once without, and every `sample_every`-th timed step
     # replays the capture with the pair (read back after that step: a device synchronisation outside the event
     # brackets).  A pair costs ~12 us inside a graph -- 2.5 % of the step -- so it is not paid on every step.
-    sample_every = max(1, min(10, args.steps // 20))
+    sample_every = max(1, min(10, args.steps // 4))  # >= 4 timed launches whenever there are >= 4 steps
     _lib.profile_captured_reset()
     use_graph = True
     try:

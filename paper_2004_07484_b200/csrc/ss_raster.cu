@@ -162,6 +162,13 @@ struct TopKShared {
     __device__ __forceinline__ float get_c(int k) const { return k < filled() ? c[k * TILE_PX] : 0.0f; }
 };
 
+#ifndef SS_RASTER_INT_CVT
+// Conversions done with integer instructions instead of F2F in the d <= 4, n_track <= 8 instantiations (bit mask:
+// 1 = r -> float64, 2 = dist^2 -> float32, 4 = r^2 - dist^2 -> float32; every combination gives the same values).
+// Measured at C3 (k_raster, us): 0: 244.6, 1: 247.5, 2: 245.4, 3: 248.3, 4: 243.7, 5: 246.4, 6: 245.8, 7: 248.0 -- the XU
+// pipe and the ALU are balanced after the other changes of the hit path, only the last one pays.
+#define SS_RASTER_INT_CVT 4
+#endif
 #ifndef SS_TOPK_SHARED
 #define SS_TOPK_SHARED 1  // K <= 8: top-K record in shared memory (1) or registers (0)
 #endif
@@ -372,13 +379,13 @@ __global__ void __launch_bounds__(TILE_PX, (KT <= 8 && DP <= 4) ? SS_RASTER_MINB
         const float rf = mi.x;
         // r^2 - dist^2 in one rounding: r is a float32 value, so r * r is exact in float64 and the fused form
         // equals the reference's (r * r) - dist2 bit for bit.  The hit path is paced by the XU pipe (conversions that
-        // touch a 64-bit value, MUFU, bit scans: 16 lanes per clock and SM) as much as by issue slots, so float -> double
-        // of a normal positive radius is done with three integer instructions instead of F2F.F64.F32.
-        // (Only where the XU pipe is the limiter -- short records at 4 CTAs per SM.  With wide payloads / long records
-        // the kernel waits on local memory instead and the extra integer instructions cost 2 %: C5 2.92 -> 2.98 ms.)
+        // touch a 64-bit value, MUFU, bit scans: 16 lanes per clock and SM) as much as by issue slots; conversions can
+        // be moved to the ALU (SS_RASTER_INT_CVT: float -> double of a normal positive radius is three integer
+        // instructions), which pays for some of them only, and only in the short-record instantiations at 4 CTAs per
+        // SM (with wide payloads / long records the kernel waits on local memory: C5 2.92 -> 2.98 ms with all three).
         constexpr bool kXuDiet = KT <= 8 && DP <= 4;
         double rd = (double)rf;
-        if (kXuDiet) {
+        if (kXuDiet && (SS_RASTER_INT_CVT & 1)) {
             const unsigned rb = __float_as_uint(rf);
             rd = __hiloint2double((int)((rb >> 3) + 0x38000000u), (int)(rb << 29));
             // zero / subnormal radius: the exact conversion (never at sane scales; volatile so that the compiler
@@ -399,9 +406,10 @@ __global__ void __launch_bounds__(TILE_PX, (KT <= 8 && DP <= 4) ? SS_RASTER_MINB
             // float64 -> float32 conversions are integer truncations (ALU) instead of F2F (XU pipe).
             // (the other instantiations convert with F2F rounding towards zero: the same values bit for bit, so that
             // n_track = 8 / 16 / 32 render identical images, reference tests/test_grad.py:147-164)
-            const float d2f = fmaxf(kXuDiet ? trunc_f64_to_f32(dist2) : __double2float_rz(dist2), 1e-37f);
-            float hc2f = kXuDiet ? trunc_f64_to_f32(hc2) : __double2float_rz(hc2);
-            if (!kXuDiet && hc2f < 1.17549435e-38f) hc2f = 0.0f;
+            constexpr bool kIntD2 = kXuDiet && (SS_RASTER_INT_CVT & 2), kIntHc = kXuDiet && (SS_RASTER_INT_CVT & 4);
+            const float d2f = fmaxf(kIntD2 ? trunc_f64_to_f32(dist2) : __double2float_rz(dist2), 1e-37f);
+            float hc2f = kIntHc ? trunc_f64_to_f32(hc2) : __double2float_rz(hc2);
+            if (!kIntHc && hc2f < 1.17549435e-38f) hc2f = 0.0f;
             const float cl = hc2f * mi.z * rcp_approx(fmaf(d2f, rsqrt_approx(d2f), rf));
             const float e2 = zzf * (mi.y * inv_g2);
             if (e2 > m2) {  // online form of raster.py:382-387

@@ -588,12 +588,12 @@ cudaError_t launch_project(const FwdLaunch &a, bool records_only, cudaStream_t s
 #ifndef SS_SORT_FORK
 #define SS_SORT_FORK 1
 #endif
-// Two side streams + fork / join events per host thread and device, created on first use and kept for the life of
+// One side stream + fork / join events per host thread and device, created on first use and kept for the life of
 // the thread (the only CUDA objects this library owns).  Per THREAD: an event re-recorded by another thread between
 // this thread's record and wait would hand the wait the wrong dependency.
 struct SideStreams {
-    cudaStream_t s1 = nullptr, s2 = nullptr;
-    cudaEvent_t fork = nullptr, join1 = nullptr, join2 = nullptr;
+    cudaStream_t s1 = nullptr;
+    cudaEvent_t fork = nullptr, join1 = nullptr;
     bool ok = false, tried = false;
 };
 static SideStreams *side_streams() {
@@ -604,10 +604,8 @@ static SideStreams *side_streams() {
     if (!x.tried) {
         x.tried = true;
         x.ok = cudaStreamCreateWithFlags(&x.s1, cudaStreamNonBlocking) == cudaSuccess &&
-               cudaStreamCreateWithFlags(&x.s2, cudaStreamNonBlocking) == cudaSuccess &&
                cudaEventCreateWithFlags(&x.fork, cudaEventDisableTiming) == cudaSuccess &&
-               cudaEventCreateWithFlags(&x.join1, cudaEventDisableTiming) == cudaSuccess &&
-               cudaEventCreateWithFlags(&x.join2, cudaEventDisableTiming) == cudaSuccess;
+               cudaEventCreateWithFlags(&x.join1, cudaEventDisableTiming) == cudaSuccess;
         if (!x.ok) (void)cudaGetLastError();
     }
     return x.ok ? &x : nullptr;
@@ -638,17 +636,18 @@ cudaError_t launch_binning(const FwdLaunch &a, cudaStream_t s) {
                                         (const unsigned long long *)(ws + L.key), tile_start, (int *)(ws + L.tile_count),
                                         pair_key, pair_id, L.ntx, status);
         }
-        // The three sort kernels work on disjoint tiles (segments of <= 512 / 513..4096 / more pairs).  The two
-        // long-segment kernels are usually a list of a few tiles or an early exit, so they run on two side streams
-        // beside the small-segment kernel (fork after k_emit, join before the raster pass; under stream capture the
-        // event waits become graph edges) instead of as two more serial steps of the frame.
+        // The small-segment kernel and the two long-segment kernels work on disjoint tiles (segments of <= 512 pairs
+        // against the list of longer ones), and the long-segment kernels are usually a list of a few tiles or an early
+        // exit, so those two run on a side stream beside the small-segment kernel (fork after k_emit, join before the
+        // raster pass; under stream capture the event waits become graph edges) instead of as two more serial steps
+        // of the frame.  k_tile_sort_mid and k_tile_sort_big stay IN ORDER on that one stream: the second one skips
+        // the list entries the first one has marked as sorted.
         SideStreams *side = SS_SORT_FORK ? side_streams() : nullptr;
         cudaStream_t s_mid = s, s_big = s;
         if (side) {
-            if (cudaEventRecord(side->fork, s) != cudaSuccess || cudaStreamWaitEvent(side->s1, side->fork, 0) != cudaSuccess ||
-                cudaStreamWaitEvent(side->s2, side->fork, 0) != cudaSuccess)
+            if (cudaEventRecord(side->fork, s) != cudaSuccess || cudaStreamWaitEvent(side->s1, side->fork, 0) != cudaSuccess)
                 return cudaGetLastError();
-            s_mid = side->s1; s_big = side->s2;
+            s_mid = side->s1; s_big = side->s1;
         }
         if (!SS_FUSED_SORT) {
             ProfScope ps(KID_SORT_SMALL, s);
@@ -686,8 +685,7 @@ cudaError_t launch_binning(const FwdLaunch &a, cudaStream_t s) {
         }
         count_launch(SS_FUSED_SORT ? 2 : 3);
         if (side) {
-            if (cudaEventRecord(side->join1, s_mid) != cudaSuccess || cudaEventRecord(side->join2, s_big) != cudaSuccess ||
-                cudaStreamWaitEvent(s, side->join1, 0) != cudaSuccess || cudaStreamWaitEvent(s, side->join2, 0) != cudaSuccess)
+            if (cudaEventRecord(side->join1, side->s1) != cudaSuccess || cudaStreamWaitEvent(s, side->join1, 0) != cudaSuccess)
                 return cudaGetLastError();
         }
     }

@@ -194,6 +194,40 @@ def test_long_tile_lists_use_the_big_sort_paths(engine):
         assert np.array_equal(f["ids"].permute(1, 2, 0).cpu().numpy(), ref["ids"])
 
 
+def test_many_long_tiles_beside_short_ones_sort_exactly_every_time(engine):
+    """The small-segment sort runs beside the two long-segment kernels (side stream), and the second long-segment kernel
+    skips the list entries the first one has marked: 64 tiles of ~1 500 candidates (k_tile_sort_mid), one tile beyond
+    4 096 (k_tile_sort_big) and short tiles in one frame, five frames in a row, lists equal to the oracle's each time."""
+    from oracle import oracle as orc
+    from paper_2004_07484_b200 import CameraSpec, camera_from_vector
+    rng = np.random.default_rng(21)
+    vec = [0, 0, 0, 0, 0, 0, 5.0, 2.0]
+    w = h = 256
+    ocam = orc.camera_from_vector(vec, w, h)
+    # a dense 128 x 128 px patch (64 tiles), a pile on one tile, a sparse rest
+    def patch(n, lo, hi, z=(10, 40)):
+        zz = rng.uniform(*z, n)
+        sx = rng.uniform(lo, hi, n) * zz / 5.0
+        sy = rng.uniform(lo, hi, n) * zz / 5.0
+        return np.column_stack([sx, sy, zz])
+    half = 1.0  # sensor half-width: sensor_w = 2 (vec[7])
+    pos = np.concatenate([patch(90_000, -0.98 * half, 0.0), patch(6_000, 0.30 * half, 0.34 * half),
+                          patch(3_000, -half, half)]).astype(np.float32)
+    m = len(pos)
+    rad = rng.uniform(0.002, 0.01, m).astype(np.float32)
+    opa = rng.uniform(0.2, 1.0, m).astype(np.float32)
+    feat = rng.uniform(0, 1, (m, 3)).astype(np.float32)
+    bg = np.zeros(3, np.float32)
+    spec = CameraSpec.from_camera(camera_from_vector(vec, w, h))
+    o_ids, o_starts = orc.tile_lists(pos, rad, ocam)
+    lens = np.diff(o_starts)
+    assert (lens > 512).sum() >= 32 and lens.max() > 4096 and (lens[lens > 0] <= 512).any(), np.sort(lens)[-5:]
+    for _ in range(5):
+        engine.forward(pos, rad, opa, feat, bg, spec, gamma=0.1, tau=0.0, collect_stats=True)
+        starts, ids = engine.tile_lists(m, 3, w, h, 5)
+        assert np.array_equal(starts, o_starts) and np.array_equal(ids, o_ids)
+
+
 def test_forward_is_deterministic_and_order_invariant(engine):
     """Bit-identical across runs (tests/test_raster.py:259-269); permuting the input spheres
     permutes the ids and leaves the image unchanged to rounding (:271-283)."""

@@ -585,10 +585,14 @@ cudaError_t launch_project(const FwdLaunch &a, bool records_only, cudaStream_t s
     return cudaGetLastError();
 }
 
+// Long-segment sort kernels on a side stream beside k_tile_sort_small (compile-time experiment, OFF): one view per step
+// gains 0.15 % graph-replayed / 1 % stream-launched (the two kernels are early exits there), but the 64-view step,
+// whose two pipeline lanes already fill the machine, loses 12 % as a graph replay (2 389 -> 2 101 frames/s: the extra
+// branches and joins of 64 forks) and 1.5 % stream-launched.
 #ifndef SS_SORT_FORK
-#define SS_SORT_FORK 1
+#define SS_SORT_FORK 0
 #endif
-// One side stream + fork / join events per host thread and device, created on first use and kept for the life of
+// Two side streams (used alternately) + fork / join events per host thread and device, created on first use and kept for the life of
 // the thread (the only CUDA objects this library owns).  Per THREAD: an event re-recorded by another thread between
 // this thread's record and wait would hand the wait the wrong dependency.
 struct SideStreams {
@@ -596,11 +600,15 @@ struct SideStreams {
     cudaEvent_t fork = nullptr, join1 = nullptr;
     bool ok = false, tried = false;
 };
+struct SideStreamPair {  // consecutive calls alternate: the two lanes of a pipelined multi-view step do not share one
+    SideStreams lane[2];
+    unsigned calls = 0;
+};
 static SideStreams *side_streams() {
-    static thread_local SideStreams per_dev[64];
+    static thread_local SideStreamPair per_dev[64];
     int dev = 0;
     if (cudaGetDevice(&dev) != cudaSuccess || dev < 0 || dev >= 64) return nullptr;
-    SideStreams &x = per_dev[dev];
+    SideStreams &x = per_dev[dev].lane[per_dev[dev].calls++ & 1u];
     if (!x.tried) {
         x.tried = true;
         x.ok = cudaStreamCreateWithFlags(&x.s1, cudaStreamNonBlocking) == cudaSuccess &&

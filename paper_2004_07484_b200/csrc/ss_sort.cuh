@@ -162,7 +162,7 @@ __device__ bool rank_ties_and_write(const unsigned *pk, int n, KeyFn keys, const
         const unsigned q = pk[p] >> IDX_BITS;
         total += (p > 0 && (pk[p - 1] >> IDX_BITS) == q) || (p + 1 < n && (pk[p + 1] >> IDX_BITS) == q);
     }
-    for (int o = 16; o > 0; o >>= 1) total += __shfl_xor_sync(0xffffffffu, total, o);
+    total = __reduce_add_sync(0xffffffffu, total);
     if (lane == 0) s_ties[warp] = total;
     __syncthreads();
     total = 0;
@@ -215,10 +215,8 @@ __device__ bool sort_packed512(int s0, int n, int np2, const SegSrc &src, int *p
             lo32 = min(lo32, (unsigned)(k1 >> 32)); hi32 = max(hi32, (unsigned)(k1 >> 32));
         }
     }
-    for (int o = 16; o > 0; o >>= 1) {
-        lo32 = min(lo32, __shfl_xor_sync(0xffffffffu, lo32, o));
-        hi32 = max(hi32, __shfl_xor_sync(0xffffffffu, hi32, o));
-    }
+    lo32 = __reduce_min_sync(0xffffffffu, lo32);  // (REDUX: one instruction each instead of a 5-step butterfly)
+    hi32 = __reduce_max_sync(0xffffffffu, hi32);
     if (lane == 0) { s_min[warp] = lo32; s_max[warp] = hi32; }
     __syncthreads();
 #pragma unroll

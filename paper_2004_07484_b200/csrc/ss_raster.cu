@@ -649,10 +649,8 @@ __global__ void __launch_bounds__(TILE_PX, (KT <= 8 && DP <= 4) ? SS_RASTER_MINB
     if (a.collect_stats) {
         unsigned h = n_hits;
         unsigned st = (valid && done) ? 1u : 0u;
-        for (int o = 16; o > 0; o >>= 1) {
-            h += __shfl_xor_sync(0xffffffffu, h, o);
-            st += __shfl_xor_sync(0xffffffffu, st, o);
-        }
+        h = __reduce_add_sync(0xffffffffu, h);
+        st = __reduce_add_sync(0xffffffffu, st);
         __syncthreads();
         if (lane == 0) {
             atomicAdd(&s_stat[1], (unsigned long long)h);

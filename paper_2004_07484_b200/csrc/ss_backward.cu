@@ -108,7 +108,20 @@ __device__ __forceinline__ void det_emit(const BackArgs &a, int id, const float 
 // partial rows in shared memory, direct-mapped by a hash of the sphere id: a group leader adds its sums to the
 // cached row of its sphere (plain shared-memory read-modify-write: one owner lane per row and instruction, the warp
 // runs the slots in lockstep) and only an evicted or finally flushed row goes to the L2 as reductions.
-constexpr int CACHE_ROWS = 64;
+// Rows per warp cache (8 .. 64) and resident CTAs per SM of the any-K instantiations.  Measured at C5 (k_backward, ms):
+// 64 rows / 2 CTAs 3.71, 32 / 2: 3.59, 32 / 3: 3.49, 16 / 3: 3.37, 8 / 3: 3.39, no cache / 3: 4.37, 16 / 4 (64 registers,
+// spills): 4.81 -- a smaller cache still catches the repeats of neighbouring slots, and the shared memory it gives back
+// goes to the L1 that serves the record and feature gathers; 80 registers hold the kernel without spills.
+#ifndef SS_BWD_CACHE_ROWS
+#define SS_BWD_CACHE_ROWS 16
+#endif
+#ifndef SS_BWD_CACHE
+#define SS_BWD_CACHE 1
+#endif
+#ifndef SS_BWD_ANYK_MINB
+#define SS_BWD_ANYK_MINB 3    // resident CTAs per SM the any-K instantiation (d <= 16) is compiled for
+#endif
+constexpr int CACHE_ROWS = SS_BWD_CACHE_ROWS;
 template <int DP>
 constexpr int cache_stride() { return (8 + ((DP + 3) & ~3)) % 8 == 0 ? 8 + ((DP + 3) & ~3) + 4 : 8 + ((DP + 3) & ~3); }
 struct RowCache {
@@ -213,8 +226,9 @@ __device__ __forceinline__ void slot_gradient_acoef(const BackArgs &a, const Rec
     if (CACHE) {
         // one owner per cache row and instruction: leaders whose spheres hash to the same row are ranked, the
         // lowest lane uses the cache, the others (rare) reduce straight into the L2
-        const unsigned h = lead ? ((unsigned)id * 2654435761u) >> 26 : (unsigned)CACHE_ROWS + lane;
-        static_assert(CACHE_ROWS == 64, "the hash keeps 6 bits");
+        constexpr int kHashShift = CACHE_ROWS == 64 ? 26 : CACHE_ROWS == 32 ? 27 : CACHE_ROWS == 16 ? 28 : 29;
+        const unsigned h = lead ? ((unsigned)id * 2654435761u) >> kHashShift : (unsigned)CACHE_ROWS + lane;
+        static_assert(CACHE_ROWS == 64 || CACHE_ROWS == 32 || CACHE_ROWS == 16 || CACHE_ROWS == 8, "6 .. 3 hash bits");
         const unsigned same = __match_any_sync(0xffffffffu, h);
         const bool owner = lead && (same & ((1u << lane) - 1u)) == 0u;
         if (owner) {
@@ -274,7 +288,7 @@ __device__ __forceinline__ void slot_gradient(const BackArgs &a, const Rec &rc, 
 // KT > 0: the K <= KT slots of a pixel are unrolled, every load of a phase issued before its first use
 // (the kernel is latency-bound on dependent gathers).  KT == 0: any K, slot by slot.
 template <int DP, int MODE, int KT>
-__global__ void __launch_bounds__(TILE_PX, (KT > 0) ? (KT <= 5 ? 4 : 3) : (DP <= 16 ? 2 : 1)) k_backward(BackArgs a) {
+__global__ void __launch_bounds__(TILE_PX, (KT > 0) ? (KT <= 5 ? 4 : 3) : (DP <= 16 ? SS_BWD_ANYK_MINB : 1)) k_backward(BackArgs a) {
     const Cam &cam = a.cam;
     const int tile = blockIdx.x;
     const int tid = threadIdx.x;
@@ -383,7 +397,9 @@ __global__ void __launch_bounds__(TILE_PX, (KT > 0) ? (KT <= 5 ? 4 : 3) : (DP <=
         cache.rows = s_uf + (size_t)K * TILE_PX + (size_t)warp * (CACHE_ROWS * CSTRIDE + CACHE_ROWS);
         cache.tag = reinterpret_cast<int *>(cache.rows + CACHE_ROWS * CSTRIDE);
         if (kMerge) {
-            cache.tag[lane] = -1; cache.tag[lane + 32] = -1;
+#pragma unroll
+            for (int r = 0; r < (CACHE_ROWS + 31) / 32; ++r)
+                if (lane + 32 * r < CACHE_ROWS) cache.tag[lane + 32 * r] = -1;
             __syncwarp();
         }
         const bool quads = (d & 3) == 0 && (reinterpret_cast<unsigned long long>(a.feat) & 15ull) == 0ull;
@@ -431,15 +447,15 @@ __global__ void __launch_bounds__(TILE_PX, (KT > 0) ? (KT <= 5 ? 4 : 3) : (DP <=
                 uf = s_uf[k * TILE_PX + tid];
             }
             const float E1 = ex2_approx_f((rc.o * zk1 * inv_g - ld) * 1.4426950408889634f);
-            slot_gradient_acoef<DP, MODE, kMerge, kMerge>(a, rc, id, zk1, ck1, E1, inv_g, up, uf - ufh, d, xs, ys, ux,
+            slot_gradient_acoef<DP, MODE, kMerge, kMerge && (SS_BWD_CACHE != 0)>(a, rc, id, zk1, ck1, E1, inv_g, up, uf - ufh, d, xs, ys, ux,
                                                           uy, uz, inv_vnorm, &cache);
         }
-        if (kMerge && !a.det) {  // flush the cache: every lane owns two rows
+        if (kMerge && SS_BWD_CACHE && !a.det) {  // flush the cache: every lane owns two rows
             __syncwarp();
 #pragma unroll
-            for (int r = 0; r < 2; ++r) {
+            for (int r = 0; r < (CACHE_ROWS + 31) / 32; ++r) {
                 const int h = lane + 32 * r;
-                const int tag = cache.tag[h];
+                const int tag = h < CACHE_ROWS ? cache.tag[h] : -1;
                 if (tag >= 0) {
                     const float4 *crow = reinterpret_cast<const float4 *>(cache.rows + h * CSTRIDE);
                     float *erow = a.raw + (size_t)tag * a.raw_stride;

@@ -369,7 +369,7 @@ __global__ void __launch_bounds__(TILE_PX, (KT <= 8 && DP <= 4) ? SS_RASTER_MINB
         }
         // dist2 is NOT clamped at zero here (raster.py:311 clamps): a slightly negative value (ray through the
         // centre, cancellation noise ~1e-13) leaves the decision hc2 > 0 and every float32 consumer unchanged
-        // (d2f is clamped below, (float)hc2 rounds to (float)r^2); only the rare t <= 0 branch needs the clamp.
+        // (d2f is clamped below, the float32 value of hc2 is that of r^2); only the rare t <= 0 branch needs the clamp.
         double t, dist2, zeta;
         if (MODE == SS_MODE_PINHOLE) {
             t = ux * cxy.x + uy * cxy.y + uz * czn.x;
@@ -407,10 +407,10 @@ __global__ void __launch_bounds__(TILE_PX, (KT <= 8 && DP <= 4) ? SS_RASTER_MINB
             const float zeta_f = (float)zeta;
             const float zzf = fmaxf(fminf(a.far_f - zeta_f, a.fmn_f), 0.0f) * a.inv_range_f;
             // closeness 1 - dist/r as (r^2 - dist^2) / (r (r + dist)): no cancellation near the rim (1 - dist / r in
-            // float32 has an ABSOLUTE error of 2e-7, which a hard-gamma stack turns into 1e-4 of the image).  The two
-            // float64 -> float32 conversions are integer truncations (ALU) instead of F2F (XU pipe).
-            // (the other instantiations convert with F2F rounding towards zero: the same values bit for bit, so that
-            // n_track = 8 / 16 / 32 render identical images, reference tests/test_grad.py:147-164)
+            // float32 has an ABSOLUTE error of 2e-7, which a hard-gamma stack turns into 1e-4 of the image).  Both
+            // float64 -> float32 conversions go TOWARDS ZERO, either as F2F.RZ (XU pipe) or as an integer truncation
+            // (ALU; SS_RASTER_INT_CVT picks per value): the same bits in every instantiation, so that n_track = 8 / 16 /
+            // 32 render identical images (reference tests/test_grad.py:147-164).
             constexpr bool kIntD2 = kXuDiet && (SS_RASTER_INT_CVT & 2), kIntHc = kXuDiet && (SS_RASTER_INT_CVT & 4);
             const float d2f = fmaxf(kIntD2 ? trunc_f64_to_f32(dist2) : __double2float_rz(dist2), 1e-37f);
             float hc2f = kIntHc ? trunc_f64_to_f32(hc2) : __double2float_rz(hc2);

@@ -415,9 +415,19 @@ def main():
     sess.set_scene(pos, rad, opa, feat, bg)
     sess.h_upstream.copy_(upstreams[local[0]].cpu())
     compact = world == 1  # the allreduced buffer of a multi-GPU step is dense
-    e2e_value = timed(lambda: sess.render_step(local_cams, gamma=GAMMA, eps=EPS, tau=TAU, reduce_fn=reduce_fn,
-                                               compact=compact), e2e_steps)
+    e2e_stream = timed(lambda: sess.render_step(local_cams, gamma=GAMMA, eps=EPS, tau=TAU, reduce_fn=reduce_fn,
+                                                compact=compact), e2e_steps)
     h2d_b, d2h_b = sess.bytes_per_step(len(local_cams))
+    # one view per step on one GPU: the same call with graph=True -- launches and copies of the step captured once and
+    # replayed (the host needs 0.15 ms to enqueue them one by one, during which the GPU waits between the short
+    # kernels of the forward pass); every other combination has no captured form and keeps the stream-launched figure
+    e2e_graphed = world == 1 and len(local_cams) == 1
+    if e2e_graphed:
+        e2e_value = timed(lambda: sess.render_step(local_cams, gamma=GAMMA, eps=EPS, tau=TAU, compact=True, graph=True),
+                          e2e_steps)
+        h2d_b, d2h_b = sess.bytes_per_step(len(local_cams))
+    else:
+        e2e_value = e2e_stream
     # (2) the same session re-uploading the whole scene and downloading all M gradient rows every step
     #     (what round 1 reported as e2e: a scene that changes on the host between steps)
     e2e_dense = timed(lambda: sess.render_step(local_cams, gamma=GAMMA, eps=EPS, tau=TAU, reduce_fn=reduce_fn,
@@ -522,7 +532,11 @@ def main():
             "clocks": clocks,
             "e2e": {"value": e2e_value, "unit": "frames/s", "h2d_bytes_per_step": h2d_b, "d2h_bytes_per_step": d2h_b,
                     "steps": e2e_steps,
-                    "path": "HostRenderSession.render_step (C ABI, pinned host buffers): scene resident on the device "
+                    "stream_launched_value": e2e_stream,
+                    "graph_replay": bool(e2e_graphed),
+                    "path": ("[the step's launches and copies replayed from one CUDA graph, render_step(graph=True); "
+                             "stream_launched_value is the same step enqueued call by call] " if e2e_graphed else "") +
+                            "HostRenderSession.render_step (C ABI, pinned host buffers): scene resident on the device "
                             "(uploaded by set_scene when it changes), argument blocks prepared once; per step and view upstream "
                             "H2D, ss_forward (last view: ss_forward_banded, 4 bands of tile rows, each band's image rows "
                             "downloaded as soon as its event completes), image D2H, ss_backward; then " +

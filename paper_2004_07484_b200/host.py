@@ -85,9 +85,17 @@ class CompactGradients:
         self._last_count = None
         self.last_bytes = 0
 
-    def gather(self, grads: dict, stream) -> dict:
-        """grads: dense device gradients (d_pos, d_rad, d_opa, d_feat, pixel_count).  Returns pinned host views
-        of `count` rows after synchronising `stream`."""
+    def estimate(self) -> int:
+        """Rows downloaded speculatively together with the count: what the previous call needed + 5 %, rounded up to
+        whole blocks of 4096 rows (a captured step bakes this size in: it should not change from step to step)."""
+        if self._last_count is None:
+            return 0
+        est = int(self._last_count * 1.05) + 1024
+        return min(self.m, (est + 4095) // 4096 * 4096)
+
+    def enqueue(self, grads: dict, stream, est: int) -> None:
+        """Device side of `gather` (no host synchronisation: capturable): mask, compaction into records, download of
+        the count and of the first `est` records."""
         m, d, words = self.m, self.d, self.words
         sp = C.c_void_p(stream.cuda_stream)
         rc = self.lib.ss_mask_nonzero_i32(_ptr(grads["pixel_count"]), m, _ptr(self.keep), sp)
@@ -107,10 +115,14 @@ class CompactGradients:
             _raise_for(rc)
         # One round trip instead of two: the count travels together with a SPECULATIVE download of as many rows as
         # the previous call needed (+5 %); only when this call touched more spheres is the remainder fetched.
-        est = min(m, int(self._last_count * 1.05) + 1024) if self._last_count is not None else 0
         self.h_count.copy_(self.count, non_blocking=True)
         if est:
             self.h_rec[: est * words].copy_(self.d_rec[: est * words], non_blocking=True)
+
+    def finish(self, stream, est: int) -> dict:
+        """Host side of `gather`: waits for `stream`, fetches the rows beyond the speculative download if there are
+        any, returns the pinned host views."""
+        words = self.words
         stream.synchronize()
         n = int(self.h_count[0])
         if n > est:
@@ -122,6 +134,13 @@ class CompactGradients:
         self.last_bytes = 8 + 4 * max(n, est) * words
         return {"count": n, "index": irec[:, 0], "pixel_count": irec[:, 1], "d_pos": rec[:, 2:5], "d_rad": rec[:, 5],
                 "d_opa": rec[:, 6], "d_feat": rec[:, 7:], "records": rec}
+
+    def gather(self, grads: dict, stream) -> dict:
+        """grads: dense device gradients (d_pos, d_rad, d_opa, d_feat, pixel_count).  Returns pinned host views
+        of `count` rows after synchronising `stream`."""
+        est = self.estimate()
+        self.enqueue(grads, stream, est)
+        return self.finish(stream, est)
 
 
 class HostRenderSession:
@@ -175,6 +194,7 @@ class HostRenderSession:
         self._scene_dirty = True
         self.last_h2d_bytes = 0
         self.last_d2h_bytes = 0
+        self._step_graphs = {}  # captured single-view steps (render_step(..., graph=True)), newest last
 
     def _new_lane(self, engine, upstream):
         dev, f32 = engine.device, torch.float32
@@ -306,6 +326,69 @@ class HostRenderSession:
             main.wait_stream(st)
         return h2d
 
+    def _enqueue_single_view(self, cam, gamma, eps, tau, normalize, gate, est):
+        """Every device operation of a one-view step with a staged upstream and compact gradient rows, without a
+        host synchronisation (so that it can be captured): upstream H2D on the copy stream under the banded forward
+        pass, image rows D2H band by band, backward pass, compaction, count + speculative rows + camera block D2H."""
+        dev = self.engine.device
+        main = torch.cuda.current_stream(dev)
+        cs = self.copy_stream
+        cs.wait_stream(main)
+        with torch.cuda.stream(cs):
+            self.upstream.copy_(self.h_upstream, non_blocking=True)
+        events = self._band_events[:self.bands] if self.bands > 1 else None
+        image = self._images[0]
+        with torch.cuda.device(dev):
+            self._forward_fast(cam, gamma, eps, tau, events, main, image)
+        main.wait_stream(cs)  # backward needs the uploaded upstream
+        with torch.cuda.stream(cs):
+            if events:
+                for b, ev in enumerate(events):
+                    r0, r1 = self._band_rows[b]
+                    cs.wait_event(ev)
+                    if r1 > r0:
+                        self.h_image[r0:r1].copy_(image[r0:r1], non_blocking=True)
+            else:
+                cs.wait_stream(main)
+                self.h_image.copy_(image, non_blocking=True)
+            self._image_copied[0].record(cs)
+        with torch.cuda.device(dev):
+            self._backward_fast(cam, gamma, eps, normalize, gate, False, main)
+        self._compact.enqueue(self.out, main, est)
+        self.h_out[self.packed.cam_off:].copy_(self.d_out[self.packed.cam_off:], non_blocking=True)
+        main.wait_stream(cs)  # the copy stream rejoins: the step ends on one stream
+
+    def _render_step_graphed(self, cam, gamma, eps, tau, normalize, gate):
+        """render_step for ONE view with a staged upstream and compact rows, replayed from a CUDA graph: the ~15 launches
+        and copies of the step cost the host 0.15 ms of enqueueing, during which the GPU waits between the short
+        kernels of the forward pass; a replay is one launch.  The capture bakes in the camera, the parameters and
+        the size of the speculative row download; the last four are kept."""
+        dev = self.engine.device
+        if self._compact is None:
+            self._compact = CompactGradients(self.m, self.d, dev)
+        est = self._compact.estimate()
+        key = (bytes(cam.to_c()), float(gamma), float(eps), float(tau), bool(normalize), bool(gate), est,
+               self._lanes[0]["key"])
+        g = self._step_graphs.get(key)
+        if g is None:
+            # warm-up outside the capture (workspace, argument blocks, event handles, function attributes)
+            self._enqueue_single_view(cam, gamma, eps, tau, normalize, gate, est)
+            torch.cuda.synchronize(dev)
+            key = key[:-1] + (self._lanes[0]["key"],)
+            g = torch.cuda.CUDAGraph()
+            with torch.cuda.graph(g):
+                self._enqueue_single_view(cam, gamma, eps, tau, normalize, gate, est)
+            while len(self._step_graphs) >= 4:
+                self._step_graphs.pop(next(iter(self._step_graphs)))
+            self._step_graphs[key] = g
+        g.replay()
+        main = torch.cuda.current_stream(dev)
+        grads = self._compact.finish(main, est)
+        grads["cam_grad"] = self.h_grads["cam_grad"]
+        self.last_h2d_bytes = 4 * self.h_upstream.numel()
+        self.last_d2h_bytes = 4 * self.h_image.numel() + self._compact.last_bytes + 4 * 32
+        return self.h_image, grads
+
     def set_scene(self, pos, rad, opa, feat, bg):
         """Stage a (new) scene: uploaded by the next render_step, resident afterwards."""
         for dst, src, shape in ((self.h_pos, pos, (self.m, 3)), (self.h_rad, rad, (self.m,)),
@@ -315,7 +398,7 @@ class HostRenderSession:
         self._scene_dirty = True
 
     def render_step(self, cams, upstream_fn=None, gamma=0.1, eps=1e-2, tau=0.01, normalize=True, gate=True,
-                    check=False, reduce_fn=None, compact=False, always_upload=False, pipeline=True):
+                    check=False, reduce_fn=None, compact=False, always_upload=False, pipeline=True, graph=False):
         """One host-to-host step over one or more views of the staged scene:
         [H2D scene if set_scene was called since the last step]; per view: ss_forward, D2H image,
         [upstream_fn(view, host image) -> host upstream, else the staged h_upstream], H2D upstream, ss_backward
@@ -327,6 +410,11 @@ class HostRenderSession:
         dev = self.engine.device
         main = torch.cuda.current_stream(dev)
         h2d = 0
+        # graph=True: a one-view step with a staged upstream and compact rows is replayed from a CUDA graph (any other
+        # combination takes the stream-launched path below)
+        if (graph and len(cams) == 1 and upstream_fn is None and not check and reduce_fn is None and compact
+                and not always_upload and not self._scene_dirty):
+            return self._render_step_graphed(cams[0], gamma, eps, tau, normalize, gate)
         if self._scene_dirty or always_upload:
             self.d_in.copy_(self.h_in, non_blocking=True)
             self._scene_dirty = False

@@ -341,6 +341,44 @@ def test_host_session_matches_device_path(engine):
     assert np.array_equal(more["pixel_count"].numpy(), dense["pixel_count"][touched])
 
 
+def test_host_session_graph_replayed_step_equals_the_stream_launched_one(engine):
+    """render_step(..., graph=True): the one-view step with a staged upstream and compact rows captured once and
+    replayed; same image bits, same touched rows, same gradients as the stream-launched step, also after the scene
+    was replaced (set_scene: one stream-launched step uploads it, the replays see the new values) and for a second
+    camera (its own capture)."""
+    import torch
+    import paper_2004_07484_b200 as pk
+    from paper_2004_07484_b200.host import HostRenderSession
+    from paper_2004_07484_b200.synthetic import benchmark_scene
+    pos, rad, opa, feat, bg, vec = benchmark_scene(20000, 160, 128, seed=16)
+    spec = pk.CameraSpec.from_camera(pk.camera_from_vector(vec, 160, 128))
+    vec2 = list(vec)
+    vec2[3] += 0.05
+    spec2 = pk.CameraSpec.from_camera(pk.camera_from_vector(vec2, 160, 128))
+    sess = HostRenderSession(20000, 3, 160, 128, 5, engine=engine)
+    sess.h_upstream.copy_(torch.sign(torch.rand(128, 160, 3, generator=torch.Generator().manual_seed(3)) - 0.5))
+
+    def snapshot(image, g):
+        return (image.numpy().copy(), int(g["count"]), g["index"].numpy().copy(), g["pixel_count"].numpy().copy(),
+                {k: g[k].numpy().copy() for k in ("d_pos", "d_rad", "d_opa", "d_feat", "cam_grad")})
+
+    for scene_radius in (1.0, 0.6):
+        sess.set_scene(pos, rad * scene_radius, opa, feat, bg)
+        for cam in (spec, spec2):
+            ref = snapshot(*sess.render_step(cam, gamma=0.1, tau=0.01, compact=True))
+            ref = snapshot(*sess.render_step(cam, gamma=0.1, tau=0.01, compact=True))  # (speculative download primed)
+            for rep in range(3):
+                got = snapshot(*sess.render_step(cam, gamma=0.1, tau=0.01, compact=True, graph=True))
+                assert np.array_equal(got[0], ref[0])
+                assert got[1] == ref[1] and np.array_equal(got[2], ref[2]) and np.array_equal(got[3], ref[3])
+                for k in ref[4]:
+                    a, e = got[4][k], ref[4][k]
+                    if k == "cam_grad":
+                        a, e = a[:14], e[:14]
+                    grad_close(a, e, f"graph-replayed {k}", rtol=2e-5)
+    assert 1 <= len(sess._step_graphs) <= 4
+
+
 def test_accumulator_reuse_protocol(engine):
     """ss_backward re-zeroes only the accumulator rows it touched and trusts a tag on the next call.
     Repeated calls, a layout change in between, and a fresh engine must all give the same gradients."""

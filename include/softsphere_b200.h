@@ -299,7 +299,10 @@ int ss_compact_workspace_bytes(int64_t M, size_t *out_bytes);
 
 /* Stable compaction of up to 16 columns by `keep` (M bytes, device) into their dst buffers (capacity M
  * rows each, must not alias src); count_out (device int64) receives the number of kept rows.  `cols` is
- * a HOST array. */
+ * a HOST array.  Columns that interleave into one array of records (equal dst strides, the columns tiling a
+ * record of <= 48 words without gaps) are assembled per block in shared memory and written as whole 128-byte lines;
+ * for that form dst and count_out may also be MAPPED PINNED HOST memory (the pass then is the download: the records
+ * are written over PCIe as the kernel runs and are valid on the host once the stream has been synchronised). */
 int ss_compact_rows(const uint8_t *keep, int64_t M, const SsColumn *cols, int32_t n_cols, void *workspace,
                     size_t workspace_bytes, int64_t *count_out, void *stream);
 

@@ -147,6 +147,52 @@ __global__ void __launch_bounds__(CB) k_compact_rows(const unsigned char *__rest
     }
 }
 
+// Columns that interleave into ONE array of records (equal destination strides, the columns tiling a record without
+// gaps): the block assembles its kept rows as records in shared memory and writes them as one contiguous run, each
+// warp store covering one aligned 128-byte line.  Into device memory this saves the strided partial-sector writes of
+// the column-by-column pass; into MAPPED PINNED HOST memory it is what makes the pass usable as the download itself
+// (full-line PCIe writes, no staging array and no separate copy: HostRenderSession's compact gradient rows).
+// cols.stride[c] holds the column's word offset inside the record here; S = words per record.
+__global__ void __launch_bounds__(CB) k_compact_records(const unsigned char *__restrict__ keep, long long M,
+                                                        const int *__restrict__ block_offset, Columns cols,
+                                                        unsigned *__restrict__ base, int S) {
+    extern __shared__ unsigned s_rec[];  // CB * S words
+    __shared__ int s_src[CB];
+    __shared__ int s_warp[CB / 32];
+    const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
+    const long long row0 = (long long)blockIdx.x * CB;
+    const long long i = row0 + tid;
+    const bool k = i < M && keep[i];
+    const unsigned bal = __ballot_sync(0xffffffffu, k);
+    if (lane == 0) s_warp[wid] = __popc(bal);
+    __syncthreads();
+    int before = 0, total = 0;
+#pragma unroll
+    for (int w = 0; w < CB / 32; ++w) {
+        const int c = s_warp[w];
+        if (w < wid) before += c;
+        total += c;
+    }
+    if (k) s_src[before + __popc(bal & ((1u << lane) - 1u))] = tid;
+    __syncthreads();
+    for (int c = 0; c < cols.n; ++c) {
+        const int w = cols.words[c];
+        const unsigned *src = cols.src[c] + (size_t)row0 * w;
+        const int off = cols.stride[c];
+        const int n_words = total * w;
+        for (int e = tid; e < n_words; e += CB) {
+            const int r = e / w, j = e - r * w;
+            s_rec[r * S + off + j] = src[s_src[r] * w + j];
+        }
+    }
+    __syncthreads();
+    unsigned *dst = base + (size_t)block_offset[blockIdx.x] * S;
+    const int n = total * S;
+    const int a = (int)(((size_t)dst >> 2) & 31);  // word offset of the run inside its first 128-byte line
+    for (int e = tid - a; e < n; e += CB)
+        if (e >= 0) dst[e] = s_rec[e];
+}
+
 __constant__ float c_fcc[12][3] = {{1, 1, 0},  {1, -1, 0}, {-1, 1, 0},  {-1, -1, 0}, {1, 0, 1},  {1, 0, -1},
                                    {-1, 0, 1}, {-1, 0, -1}, {0, 1, 1},  {0, 1, -1},  {0, -1, 1}, {0, -1, -1}};
 
@@ -285,9 +331,36 @@ int ss_compact_rows(const uint8_t *keep, int64_t M, const SsColumn *cols, int32_
     }
     const int n_blocks = (int)((M + CB - 1) / CB);
     int *bc = (int *)workspace;
+    // interleaved destination?  (every column with the same stride S, the columns tiling [base, base + S words))
+    int S = n_cols > 0 ? c.stride[0] : 0;
+    unsigned *base = n_cols > 0 ? c.dst[0] : nullptr;
+    bool records = n_cols > 1 && S <= 48;
+    int covered = 0;
+    for (int i = 0; i < n_cols && records; ++i) {
+        records = c.stride[i] == S;
+        if (c.dst[i] < base) base = c.dst[i];
+        covered += c.words[i];
+    }
+    records = records && covered == S;
+    if (records) {
+        unsigned long long used = 0;  // S <= 48 words: one bit per word of the record
+        for (int i = 0; i < n_cols && records; ++i) {
+            const long long off = c.dst[i] - base;
+            if (off < 0 || off + c.words[i] > S) { records = false; break; }
+            const unsigned long long m = ((c.words[i] >= 64 ? 0ull : (1ull << c.words[i])) - 1ull) << off;
+            if (used & m) records = false;
+            used |= m;
+        }
+    }
     k_compact_count<<<n_blocks, CB, 0, s>>>(keep, M, bc);
     k_compact_scan<<<1, 1024, 0, s>>>(bc, n_blocks, (long long *)count_out);
-    k_compact_rows<<<n_blocks, CB, 0, s>>>(keep, M, bc, c);
+    if (records) {
+        Columns r = c;
+        for (int i = 0; i < n_cols; ++i) r.stride[i] = (int)(c.dst[i] - base);
+        k_compact_records<<<n_blocks, CB, (size_t)CB * S * sizeof(unsigned), s>>>(keep, M, bc, r, base, S);
+    } else {
+        k_compact_rows<<<n_blocks, CB, 0, s>>>(keep, M, bc, c);
+    }
     count_launch(3);
     return rc_of(cudaGetLastError());
 }

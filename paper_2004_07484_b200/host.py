@@ -17,6 +17,7 @@ Transfers are packed and minimal:
 from __future__ import annotations
 
 import ctypes as C
+import os
 
 import numpy as np
 import torch
@@ -66,11 +67,17 @@ class CompactGradients:
     [index i32 | pixel_count i32 | d_pos 3 | d_rad | d_opa | d_feat d] (7 + d words each) and downloaded with a
     single copy; the host views are columns of that record array."""
 
-    def __init__(self, num_spheres: int, feature_dim: int, device):
+    def __init__(self, num_spheres: int, feature_dim: int, device, zero_copy=None):
         m, d = int(num_spheres), int(feature_dim)
         self.m, self.d, self.device = m, d, device
         self.lib = _lib.load()
         self.words = 7 + d
+        # zero_copy: the compaction kernel writes the records (and the count) straight into the pinned host array
+        # -- whole 128-byte lines over PCIe while it runs -- instead of into a device array that a copy then
+        # downloads: no staging pass, no speculative size, never a second round trip.  SS_COMPACT_ZERO_COPY=0/1.
+        if zero_copy is None:
+            zero_copy = os.environ.get("SS_COMPACT_ZERO_COPY", "1") != "0"
+        self.zero_copy = bool(zero_copy)
         self.index = torch.arange(m, dtype=torch.int32, device=device)  # one-time iota (source of the index column)
         self.keep = torch.empty(max(m, 1), dtype=torch.uint8, device=device)
         self.count = torch.zeros(1, dtype=torch.int64, device=device)
@@ -88,6 +95,8 @@ class CompactGradients:
     def estimate(self) -> int:
         """Rows downloaded speculatively together with the count: what the previous call needed + 5 %, rounded up to
         whole blocks of 4096 rows (a captured step bakes this size in: it should not change from step to step)."""
+        if self.zero_copy:
+            return self.m  # (nothing is downloaded speculatively: the kernel writes exactly `count` records)
         if self._last_count is None:
             return 0
         est = int(self._last_count * 1.05) + 1024
@@ -105,14 +114,18 @@ class CompactGradients:
                 (grads["d_opa"], 1), (grads["d_feat"], d))
         arr = (_lib.SsColumn * len(cols))()
         off = 0
+        rec_ptr = self.h_rec.data_ptr() if self.zero_copy else self.d_rec.data_ptr()
+        count = self.h_count if self.zero_copy else self.count
         for i, (src, w) in enumerate(cols):  # interleave the columns into records: dst offset inside the first record
-            arr[i].src, arr[i].dst = src.data_ptr(), self.d_rec.data_ptr() + 4 * off
+            arr[i].src, arr[i].dst = src.data_ptr(), rec_ptr + 4 * off
             arr[i].row_bytes, arr[i].dst_stride_bytes = 4 * w, 4 * words
             off += w
         rc = self.lib.ss_compact_rows(_ptr(self.keep), m, arr, len(cols), _ptr(self.ws), self.ws.numel(),
-                                      _ptr(self.count), sp)
+                                      _ptr(count), sp)
         if rc != _lib.SS_OK:
             _raise_for(rc)
+        if self.zero_copy:
+            return
         # One round trip instead of two: the count travels together with a SPECULATIVE download of as many rows as
         # the previous call needed (+5 %); only when this call touched more spheres is the remainder fetched.
         self.h_count.copy_(self.count, non_blocking=True)
@@ -131,7 +144,7 @@ class CompactGradients:
         self._last_count = n
         rec = self.h_rec[: n * words].view(n, words)
         irec = rec.view(torch.int32)
-        self.last_bytes = 8 + 4 * max(n, est) * words
+        self.last_bytes = 8 + 4 * (n if self.zero_copy else max(n, est)) * words
         return {"count": n, "index": irec[:, 0], "pixel_count": irec[:, 1], "d_pos": rec[:, 2:5], "d_rad": rec[:, 5],
                 "d_opa": rec[:, 6], "d_feat": rec[:, 7:], "records": rec}
 

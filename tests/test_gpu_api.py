@@ -341,6 +341,33 @@ def test_host_session_matches_device_path(engine):
     assert np.array_equal(more["pixel_count"].numpy(), dense["pixel_count"][touched])
 
 
+@pytest.mark.parametrize("m,d", [(1, 3), (255, 1), (4099, 3), (100000, 16), (20000, 32)])
+def test_compact_gradient_records_device_array_and_mapped_host_array(engine, m, d):
+    """CompactGradients: records [index | pixel_count | d_pos | d_rad | d_opa | d_feat] of the rows with pixel_count > 0,
+    bit-identical to the dense columns, for the device record array + copy (zero_copy=False) and for the compaction
+    kernel writing into the mapped pinned host array (zero_copy=True); ragged block ends, empty and full masks."""
+    import torch
+    from paper_2004_07484_b200.host import CompactGradients
+    dev = engine.device
+    g = torch.Generator().manual_seed(m + d)
+    for density in (0.0, 0.3, 1.0):
+        pc = ((torch.rand(m, generator=g) < density).to(torch.int32) * torch.randint(1, 900, (m,), generator=g,
+                                                                                     dtype=torch.int32))
+        dense = {"pixel_count": pc, "d_pos": torch.randn(m, 3, generator=g), "d_rad": torch.randn(m, generator=g),
+                 "d_opa": torch.randn(m, generator=g), "d_feat": torch.randn(m, d, generator=g)}
+        on_dev = {k: v.to(dev) for k, v in dense.items()}
+        touched = np.flatnonzero(pc.numpy() > 0)
+        for zero_copy in (False, True):
+            cg = CompactGradients(m, d, dev, zero_copy=zero_copy)
+            for rep in range(2):  # (the second call of the copying form downloads speculatively)
+                got = cg.gather(on_dev, torch.cuda.current_stream(dev))
+                assert got["count"] == touched.size
+                assert np.array_equal(got["index"].numpy(), touched)
+                for k in ("pixel_count", "d_pos", "d_rad", "d_opa", "d_feat"):
+                    assert np.array_equal(got[k].numpy(), dense[k].numpy()[touched]), (k, zero_copy, density)
+                assert cg.last_bytes >= 8 + 4 * touched.size * (7 + d)
+
+
 def test_host_session_graph_replayed_step_equals_the_stream_launched_one(engine):
     """render_step(..., graph=True): the one-view step with a staged upstream and compact rows captured once and
     replayed; same image bits, same touched rows, same gradients as the stream-launched step, also after the scene

@@ -540,8 +540,9 @@ def main():
                             "(uploaded by set_scene when it changes), argument blocks prepared once; per step and view upstream "
                             "H2D, ss_forward (last view: ss_forward_banded, 4 bands of tile rows, each band's image rows "
                             "downloaded as soon as its event completes), image D2H, ss_backward; then " +
-                            ("the gradient rows of the touched spheres (index + count + grads, compacted on the device) "
-                             "+ camera block D2H" if compact else
+                            ("the gradient rows of the touched spheres (index + count + grads) compacted on the device, "
+                             "the compaction kernel writing the records straight into the mapped pinned host array "
+                             "(counted in d2h_bytes_per_step), + camera block D2H" if compact else
                              "the allreduce of the sphere gradients and one D2H block with all M gradient rows")},
             "e2e_dense_reupload": {"value": e2e_dense, "unit": "frames/s", "h2d_bytes_per_step": dense_h2d,
                                    "d2h_bytes_per_step": dense_d2h,

@@ -19,7 +19,7 @@ ncu -i $out/${tag}_full.ncu-rep --page source --csv --print-source cuda,sass > $
 python scripts/ncu_stalls.py $out/${tag}_src.csv k_raster 45 > $out/${tag}_raster_stalls.txt 2>&1
 python scripts/launch_shares.py $out/${tag}_launches.csv > $out/${tag}_launch_shares.txt 2>&1
 python scripts/run_config.py --count 10000000 --width 1920 --height 1080 --d 16 --k 32 --tau 0.01 > $out/${tag}_c5.log 2>&1
-SAN="tests/test_gpu_parity.py::test_golden_forward tests/test_gpu_parity.py::test_golden_backward tests/test_gpu_fuzz.py tests/test_gpu_api.py::test_early_stop_bound_and_chunk_sizes"
+SAN="tests/test_gpu_parity.py::test_golden_forward tests/test_gpu_parity.py::test_golden_backward tests/test_gpu_fuzz.py tests/test_gpu_api.py::test_early_stop_bound_and_chunk_sizes tests/test_gpu_api.py::test_compact_gradient_records_device_array_and_mapped_host_array"
 compute-sanitizer --tool memcheck --error-exitcode 1 python -m pytest $SAN -x -q > $out/${tag}_sanitizer_memcheck.log 2>&1
 compute-sanitizer --tool racecheck --error-exitcode 1 python -m pytest tests/test_gpu_parity.py::test_golden_forward tests/test_gpu_parity.py::test_golden_backward -x -q > $out/${tag}_sanitizer_racecheck.log 2>&1
 compute-sanitizer --tool synccheck --error-exitcode 1 python -m pytest tests/test_gpu_parity.py::test_golden_forward tests/test_gpu_parity.py::test_golden_backward -x -q > $out/${tag}_sanitizer_synccheck.log 2>&1

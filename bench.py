@@ -538,7 +538,7 @@ def main():
                              "stream_launched_value is the same step enqueued call by call] " if e2e_graphed else "") +
                             "HostRenderSession.render_step (C ABI, pinned host buffers): scene resident on the device "
                             "(uploaded by set_scene when it changes), argument blocks prepared once; per step and view upstream "
-                            "H2D, ss_forward (last view: ss_forward_banded, 4 bands of tile rows, each band's image rows "
+                            "H2D, ss_forward (last view: ss_forward_banded, 2 bands of tile rows, each band's image rows "
                             "downloaded as soon as its event completes), image D2H, ss_backward; then " +
                             ("the gradient rows of the touched spheres (index + count + grads) compacted on the device, "
                              "the compaction kernel writing the records straight into the mapped pinned host array "

@@ -9,11 +9,13 @@ Transfers are packed and minimal:
   * gradients come back either dense (ONE block: all M rows + pixel counts + the camera block) or
     `compact=True`: only the U rows of spheres that received gradient (pixel_count > 0), preceded by
     their sphere indices -- ss_mask_nonzero_i32 + ss_compact_rows on the device interleave them into one
-    array of records, downloaded with one copy together with the row count (C3: 36 MB -> 12.7 MB);
+    array of records (C3: 36 MB -> 12.7 MB), written by the compaction kernel straight into the mapped pinned
+    host array together with the row count (CompactGradients(zero_copy=True); a device array + one copy otherwise);
   * the image download runs on a second stream so that it overlaps the upstream upload (the two
     PCIe directions); the forward pass draws the image in `bands` bands of tile rows (ss_forward_banded) and
     every band is downloaded as soon as it is final -- the upper bands under the raster kernel of the lower
-    ones, the last one under the backward pass."""
+    ones, the last one under the backward pass (2 bands by default: each band is a raster launch of its own and
+    pays its own partial waves; measured 1 / 2 / 3 / 4 / 8 bands, scripts/e2e_bands.py)."""
 from __future__ import annotations
 
 import ctypes as C
@@ -158,7 +160,7 @@ class CompactGradients:
 
 class HostRenderSession:
     def __init__(self, num_spheres: int, feature_dim: int, width: int, height: int, top_k: int = 5,
-                 engine: RenderEngine = None, device="cuda", bands: int = 4):
+                 engine: RenderEngine = None, device="cuda", bands: int = 2):
         self.engine = engine or RenderEngine(device)
         dev = self.engine.device
         m, d, w, h = int(num_spheres), int(feature_dim), int(width), int(height)

@@ -207,7 +207,11 @@ int ss_backward(const SsBackwardArgs *args, void *stream);
  * ss_band_rows(height, n_bands, b) are final in image / bg_weight / ids / z / closeness / log_denom.  A host
  * caller lets a copy stream wait on event b and downloads those image rows while the later bands are still being
  * drawn (the reference returns the whole image at once, raster.py:504-512; results are identical to ss_forward:
- * tiles are independent).  The status counters are complete after the last band. */
+ * tiles are independent).  The status counters are complete after the last band.  Bands 1.. are launched on a
+ * library-owned side stream beside band 0 (fork after the binning pass, join on `stream` before the last event, which
+ * therefore marks the end of the whole pass on `stream`; graph edges under stream capture), so that their CTAs fill
+ * the partial last wave of the band before; the events of the bands in between are recorded on that side stream.
+ * SS_BAND_FORK=0 in the environment keeps every launch on `stream`. */
 #define SS_MAX_BANDS 16
 int ss_forward_banded(const SsForwardArgs *args, int n_bands, void *const *band_events, void *stream);
 int ss_band_rows(int height, int n_bands, int band, int *row_begin, int *row_end);

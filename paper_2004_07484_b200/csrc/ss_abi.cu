@@ -1,6 +1,7 @@
 // C ABI of the sphere-render hot path (see include/softsphere_b200.h).  Host-side argument
 // checks mirror the reference's exceptions; kernels are enqueued on the caller's stream and
 // nothing here allocates, frees or synchronises (except ss_read_status).
+#include <stdlib.h>
 #include <atomic>
 #include <cmath>
 #include <cstring>
@@ -251,11 +252,30 @@ static int forward_impl(const SsForwardArgs *a, int n_bands, void *const *band_e
     }
     // bands of whole tile rows, one raster launch each; the event after band b completes when rows
     // [ss_band_rows(b)) of every forward output are final (a copy stream can start downloading them)
+    // Every band is a launch of its own and would pay its own partial last wave (1 024 tiles on 592 resident CTAs are
+    // 1.7 waves).  The bands are independent, so bands 1.. are launched on a library-owned side stream (fork after the
+    // binning pass, join before the last band's event): their CTAs fill the SMs that band 0's last wave leaves idle,
+    // band b's event still completes with band b alone, and the whole pass costs about one unbanded launch.  Under
+    // stream capture the fork / join become graph edges.  SS_BAND_FORK=0: all bands in order on the caller's stream.
+    static const bool fork_bands = [] { const char *v = getenv("SS_BAND_FORK"); return !(v && v[0] == '0'); }();
+    cudaStream_t side = nullptr;
+    cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
+    const bool forked = fork_bands && n_bands > 1 && side_stream(&side, &ev_fork, &ev_join);
+    if (forked) {
+        if (cudaEventRecord(ev_fork, s) != cudaSuccess || cudaStreamWaitEvent(side, ev_fork, 0) != cudaSuccess)
+            return cuda_fail(cudaGetLastError());
+    }
     for (int b = 0; b < n_bands; ++b) {
         const int ty0 = (int)((long long)f.L.nty * b / n_bands), ty1 = (int)((long long)f.L.nty * (b + 1) / n_bands);
-        e = launch_raster(f, s, ty0 * f.L.ntx, (ty1 - ty0) * f.L.ntx);
+        cudaStream_t sb = (forked && b > 0) ? side : s;
+        e = launch_raster(f, sb, ty0 * f.L.ntx, (ty1 - ty0) * f.L.ntx);
         if (e != cudaSuccess) return cuda_fail(e);
-        e = cudaEventRecord((cudaEvent_t)band_events[b], s);
+        if (forked && b == n_bands - 1) {  // the caller's stream rejoins: its last event = the whole pass
+            if (cudaEventRecord(ev_join, side) != cudaSuccess || cudaStreamWaitEvent(s, ev_join, 0) != cudaSuccess)
+                return cuda_fail(cudaGetLastError());
+            sb = s;
+        }
+        e = cudaEventRecord((cudaEvent_t)band_events[b], sb);
         if (e != cudaSuccess) return cuda_fail(e);
     }
     return SS_OK;

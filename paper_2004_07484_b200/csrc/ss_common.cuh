@@ -155,6 +155,9 @@ cudaError_t launch_project(const FwdLaunch &a, bool records_only, cudaStream_t s
 cudaError_t launch_binning(const FwdLaunch &a, cudaStream_t s);
 // draws tiles [tile0, tile0 + n_tiles) (n_tiles < 0: to the last tile)
 cudaError_t launch_raster(const FwdLaunch &a, cudaStream_t s, int tile0 = 0, int n_tiles = -1);
+// One of this thread's two library-owned side streams (used alternately) with its fork / join events, created on
+// first use; false if they could not be created (callers then stay on their own stream).
+bool side_stream(cudaStream_t *side, cudaEvent_t *fork, cudaEvent_t *join);
 cudaError_t launch_backward(const BwdLaunch &a, cudaStream_t s);
 
 void count_launch(int n = 1);

@@ -608,15 +608,23 @@ static SideStreams *side_streams() {
     static thread_local SideStreamPair per_dev[64];
     int dev = 0;
     if (cudaGetDevice(&dev) != cudaSuccess || dev < 0 || dev >= 64) return nullptr;
-    SideStreams &x = per_dev[dev].lane[per_dev[dev].calls++ & 1u];
-    if (!x.tried) {
+    for (SideStreams &x : per_dev[dev].lane) {  // both lanes on first use (a warm-up call then covers a later capture)
+        if (x.tried) continue;
         x.tried = true;
         x.ok = cudaStreamCreateWithFlags(&x.s1, cudaStreamNonBlocking) == cudaSuccess &&
                cudaEventCreateWithFlags(&x.fork, cudaEventDisableTiming) == cudaSuccess &&
                cudaEventCreateWithFlags(&x.join1, cudaEventDisableTiming) == cudaSuccess;
         if (!x.ok) (void)cudaGetLastError();
     }
+    SideStreams &x = per_dev[dev].lane[per_dev[dev].calls++ & 1u];
     return x.ok ? &x : nullptr;
+}
+
+bool side_stream(cudaStream_t *side, cudaEvent_t *fork, cudaEvent_t *join) {
+    SideStreams *x = side_streams();
+    if (!x) return false;
+    *side = x->s1; *fork = x->fork; *join = x->join1;
+    return true;
 }
 
 cudaError_t launch_binning(const FwdLaunch &a, cudaStream_t s) {

@@ -419,7 +419,10 @@ class HostRenderSession:
         [upstream_fn(view, host image) -> host upstream, else the staged h_upstream], H2D upstream, ss_backward
         (gradients summed over the views); optional reduce_fn(out) (the multi-GPU allreduce); D2H gradients
         (dense block, or compact rows of the touched spheres).  Returns after the streams are synchronised,
-        with the last image and the gradient views (pinned host tensors)."""
+        with the last image and the gradient views (pinned host tensors).
+        graph=True: a one-view step with the staged upstream (no upstream_fn), compact rows and a resident scene is
+        replayed from a CUDA graph captured on its first use (same results; any other combination is enqueued call
+        by call as without the flag)."""
         if not isinstance(cams, (list, tuple)):
             cams = [cams]
         dev = self.engine.device

@@ -190,8 +190,10 @@ class HostRenderSession:
         # Python work before the first kernel launch is GPU idle time on this path (it was 0.1 ms of a 1 ms step)
         k = self.k
         # two image buffers, alternating by view: the download of view i must not hold back the forward of view i + 1
-        self._images = [torch.empty((h, w, d), dtype=f32, device=dev) for _ in range(2)]
-        self._image_copied = [torch.cuda.Event(), torch.cuda.Event()]
+        # (a ring of image buffers: the pipelined multi-view step uses all four, so that the forward pass of view
+        # i + 2 does not wait for the download of image i; the other paths alternate between the first two)
+        self._images = [torch.empty((h, w, d), dtype=f32, device=dev) for _ in range(4)]
+        self._image_copied = [torch.cuda.Event() for _ in range(4)]
         # "lane" j = an engine (workspace) + its forward outputs + its upstream buffer + its argument blocks.  Lane 0
         # serves single views; multi-view steps alternate views between lane 0 and lane 1 (allocated on first use)
         # on two compute streams, so the forward of view i + 1 runs under the backward of view i.
@@ -203,6 +205,7 @@ class HostRenderSession:
         self.d_out, self.h_out = self.packed.d_out, self.packed.h_out
         self._compact = None
         self.copy_stream = torch.cuda.Stream(device=dev)
+        self._upload_stream = None  # H2D stream of the pipelined multi-view step
         self.bands = max(1, int(bands))
         self._band_events = [torch.cuda.Event() for _ in range(self.bands)]
         self._band_rows = [self.engine.band_rows(h, self.bands, b) for b in range(self.bands)]
@@ -294,9 +297,13 @@ class HostRenderSession:
         if self._compute_streams is None:
             self._compute_streams = [torch.cuda.Stream(device=dev), torch.cuda.Stream(device=dev)]
         copy = self.copy_stream
+        if self._upload_stream is None:
+            self._upload_stream = torch.cuda.Stream(device=dev)
+        upload = self._upload_stream
         for st in self._compute_streams:
             st.wait_stream(main)  # scene upload / earlier work of the caller
         copy.wait_stream(main)
+        upload.wait_stream(main)
         bwd_done, last_bwd, h2d = [None, None], None, 0
         with torch.cuda.device(dev):
             for i, cam in enumerate(cams):
@@ -304,16 +311,17 @@ class HostRenderSession:
                 lane, st = self._lane(j), self._compute_streams[j]
                 last = i == len(cams) - 1
                 events = self._band_events[:self.bands] if (last and self.bands > 1) else None
-                with torch.cuda.stream(copy):  # upstream of view i -> lane j, once backward(i - 2) has consumed it
+                with torch.cuda.stream(upload):  # upstream of view i -> lane j, once backward(i - 2) has consumed it
                     if bwd_done[j] is not None:
-                        copy.wait_event(bwd_done[j])
+                        upload.wait_event(bwd_done[j])
                     lane["upstream"].copy_(self.h_upstream, non_blocking=True)
                     up_ready = torch.cuda.Event()
-                    up_ready.record(copy)
+                    up_ready.record(upload)
                 h2d += 4 * self.h_upstream.numel()
-                image = self._images[j]
-                if i > 1:  # this image buffer was last used two views ago: its download must have read it
-                    st.wait_event(self._image_copied[j])
+                r = i & 3
+                image = self._images[r]
+                if i > 3:  # this image buffer was last used four views ago: its download must have read it
+                    st.wait_event(self._image_copied[r])
                 with torch.cuda.stream(st):  # (a lane's first use initialises its workspace on the current stream)
                     self._forward_fast(cam, gamma, eps, tau, events, st, image, lane)
                 fwd_done = torch.cuda.Event()
@@ -328,7 +336,7 @@ class HostRenderSession:
                     else:
                         copy.wait_event(fwd_done)
                         self.h_image.copy_(image, non_blocking=True)
-                    self._image_copied[j].record(copy)
+                    self._image_copied[r].record(copy)
                 st.wait_event(up_ready)
                 if last_bwd is not None:
                     st.wait_event(last_bwd)
